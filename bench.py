@@ -1,0 +1,469 @@
+#!/usr/bin/env python
+"""Benchmark: blockwise NF4 dequantization on B200 (arxiv 2604.02556 hot path).
+
+A *step* is one pass of the whole hot path over a model's NF4 linear weights
+(all 7 projections of every decoder layer) -- what one inference forward
+pass dequantizes.  Default workload (N=1): BASELINE.json configs[1], the
+Gemma-3-27B linear-layer set, blocksize 64, double-quantized absmax, bf16
+output: 25.6 G elements, 64.4 GB of algorithmic traffic per step (inputs and
+outputs far larger than the 126 MB L2, so no flush is needed).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2]
+                    [--inputs gaussian|hash] [--scaling weak|strong] [--impl ours|reference]
+
+Multi-GPU (torchrun, one process per GPU): the path has no exchange step, so
+no data-path collective.  --scaling weak (default): every rank dequantizes its
+own full linear-weight set (independent replicas, seeds offset by rank);
+--scaling strong: the model is row-sharded across ranks (config 3/4 style).
+Time is measured with CUDA events on the launching stream, max over ranks.
+
+Rank 0 prints ONE JSON line.  `value` is whole-job algorithmic GB/s
+(codes ceil(n/2) + scales + 2 B/elt output), `e2e` the same metric
+through the host-buffer C-ABI call (pinned host -> HBM -> host, copies timed),
+`roofline` the dequant kernel against the measured HBM copy peak,
+`cpu_baseline` the CPU oracle on a bounded sample on this host's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from synth import inputs as syn  # noqa: E402
+from synth import workloads as wl  # noqa: E402
+
+METRIC = "NF4 dequant HBM GB/s & % of B200 peak, Gelem/s at 1/2/4/8 GPUs"
+UNIT = "GB/s"
+
+
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.gpu)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.t:
+            self.t.join(timeout=2)
+        sm, smax, power, reasons = [], 0.0, [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            parts = [p.strip() for p in l.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = max(smax, float(parts[2]))
+                power.append(float(parts[3]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": max(power) if power else None}
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle timing (cpu_baseline and the --impl reference arm)
+# ---------------------------------------------------------------------------
+def oracle_sample_inputs(cfg, n):
+    """Counter-based inputs for the first n elements of a tensor of the workload."""
+    c = wl.CONFIGS[cfg]
+    bs = c.blocksize
+    nb = -(-n // bs)
+    packed = syn.hash_packed(7, 0, (n + 1) // 2)
+    if c.dq:
+        kw = dict(qabsmax=syn.hash_qabsmax(7, 0, nb), code2=syn.dynamic_map_code2(),
+                  absmax2=syn.hash_absmax2(7, 0, -(-nb // 256)), offset=float(syn.hash_offset(7)))
+    else:
+        kw = dict(absmax=syn.hash_absmax(7, 0, nb))
+    return packed, kw
+
+
+def time_oracle(cfg, target_s=10.0, max_elems=None, threads=None):
+    """Time the oracle (as it stands) on this host's cores over a bounded sample
+    of the workload sized to ~target_s seconds.  Returns a cpu_baseline dict."""
+    import oracle
+    c = wl.CONFIGS[cfg]
+    threads = threads or len(os.sched_getaffinity(0))
+    code = oracle.OUT_F16 if c.out_dtype == "f16" else oracle.OUT_BF16
+    probe_n = 1 << 22
+    packed, kw = oracle_sample_inputs(cfg, probe_n)
+    t0 = time.perf_counter()
+    oracle.dequantize(packed, probe_n, c.blocksize, code, threads=threads, **kw)
+    rate = probe_n / max(time.perf_counter() - t0, 1e-6)
+    n = int(rate * target_s)
+    n = max(1 << 22, min(n, max_elems or (1 << 31)))
+    n -= n % 16384
+    packed, kw = oracle_sample_inputs(cfg, n)
+    t0 = time.perf_counter()
+    oracle.dequantize(packed, n, c.blocksize, code, threads=threads, **kw)
+    dt = time.perf_counter() - t0
+    bpe = wl.algorithmic_bytes_per_element(c.blocksize, c.dq)
+    return {"value": round(n * bpe / dt / 1e9, 3), "unit": UNIT, "cores": threads, "kind": "oracle",
+            "gelem_per_s": round(n / dt / 1e9, 4), "seconds": round(dt, 2),
+            "sample": f"one synthetic tensor of {n} elements with the workload blocksize, absmax mode and output dtype "
+                      f"(counter-based inputs; {c.description}), "
+                      f"{threads} threads, scalar C oracle"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    cfg = args.config
+    steps = []
+    for i in range(args.warmup + args.steps):
+        cb = time_oracle(cfg, target_s=args.ref_step_seconds)
+        if i >= args.warmup:
+            steps.append(cb)
+    v = statistics.median(s["value"] for s in steps)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": args.scaling,
+        "vs_baseline": None, "dtype": "u8->" + wl.CONFIGS[cfg].out_dtype, "data": "synthetic",
+        "config": {"workload": wl.CONFIGS[cfg].description, "key": cfg},
+        "ms_per_step": round(1000 * statistics.median(s["seconds"] for s in steps), 1),
+        "cpu_baseline": {k: steps[-1][k] for k in ("kind", "cores", "sample")} | {"value": v, "unit": UNIT},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def build_store(args, rank, world, device):
+    from paper_2604_02556_b200 import weights
+    c = wl.CONFIGS[args.config]
+    if args.scaling == "strong":
+        tensors = wl.config_tensors(args.config, world_size=world, rank=rank, layers=args.layers)
+    else:
+        tensors = wl.config_tensors(args.config, layers=args.layers)
+    seed0 = 1000 * int(args.config[-1]) + 100000 * rank
+    maker = weights.from_gaussian if args.inputs == "gaussian" else weights.from_hash
+    return maker(tensors, c.blocksize, c.dq, c.out_dtype, seed0=seed0, device=device), tensors
+
+
+def measure_sol(nf4, torch, in_bytes=2 << 30, reps=10):
+    src = torch.empty(in_bytes, dtype=torch.uint8, device="cuda")
+    src.random_(0, 255)
+    dst = torch.empty(4 * in_bytes, dtype=torch.uint8, device="cuda")
+    for _ in range(3):
+        nf4.nf4_sol_stream(src, in_bytes, dst)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    s.record()
+    for _ in range(reps):
+        nf4.nf4_sol_stream(src, in_bytes, dst)
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / reps
+    del src, dst
+    torch.cuda.empty_cache()
+    return round(5 * in_bytes / (ms * 1e-3) / 1e9, 1)
+
+
+def run_e2e(nf4, torch, ws, args, max_host_bytes):
+    """Same metric through nf4_dequantize_host: pinned host inputs -> HBM ->
+    kernel -> pinned host outputs, copies inside the timed region."""
+    c = wl.CONFIGS[args.config]
+    bs = ws.blocksize
+    # bounded prefix of the workload that fits the host-memory budget
+    chosen, host_bytes = [], 0
+    for i, e in enumerate(ws.entries):
+        nb = -(-e.n // bs)
+        b = (e.n + 1) // 2 + 2 * e.n + (nb + 4 * (-(-nb // 256)) if ws.dq else 4 * nb)
+        if chosen and host_bytes + b > max_host_bytes:
+            break
+        chosen.append(i)
+        host_bytes += b
+    chunk = 1 << 24
+    wsp = torch.empty(nf4.nf4_host_workspace_bytes(chunk, bs, ws.dq), dtype=torch.uint8, device="cuda")
+    items, h2d, d2h, alg = [], 0, 0, 0
+    code2_h = ws.code2.cpu().pin_memory() if ws.dq else None
+    for i in chosen:
+        e = ws.entries[i]
+        nb = -(-e.n // bs)
+        pk = ws.codes[e.codes_off:e.codes_off + (e.n + 1) // 2].cpu().pin_memory()
+        out = torch.empty(e.n, dtype=torch.int16).pin_memory()
+        if ws.dq:
+            q = ws.scales[e.scale_off:e.scale_off + nb].cpu().pin_memory()
+            a2 = ws.groups[e.group_off:e.group_off + 4 * (-(-nb // 256))].cpu().pin_memory()
+            dq = nf4.DQ(q, code2_h, a2, e.offset)
+            items.append((pk, None, dq, e.n, out))
+            h2d += pk.numel() + q.numel() + a2.numel() + 1024
+        else:
+            a = ws.scales[e.scale_off:e.scale_off + 4 * nb].cpu().pin_memory()
+            items.append((pk, a, None, e.n, out))
+            h2d += pk.numel() + a.numel()
+        d2h += 2 * e.n
+        alg += (e.n + 1) // 2 + 2 * e.n + ((nb + 4 * (-(-nb // 256)) + 1024) if ws.dq else 4 * nb)
+
+    def step():
+        launches = 0
+        for pk, a, dq, n, out in items:
+            nf4.nf4_dequantize_host(pk, a, dq, n=n, blocksize=bs, out_dtype=ws.out_dtype, out=out,
+                                    workspace=wsp, chunk_elems=chunk)
+            launches += nf4.nf4_last_launch_count()
+        return launches
+
+    for _ in range(2):
+        step()
+    k = args.e2e_steps
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(k):
+        step()
+    dt = (time.perf_counter() - t0) / k
+    del wsp
+    return {"value": round(alg / dt / 1e9, 2), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": round(dt * 1e3, 2),
+            "gelem_per_s": round(sum(it[3] for it in items) / dt / 1e9, 3),
+            "sample": f"first {len(chosen)} of {len(ws.entries)} tensors "
+                      f"({sum(it[3] for it in items) / 1e9:.2f} G elements) through nf4_dequantize_host, "
+                      f"pinned host buffers, {chunk}-element chunks"}
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2604_02556_b200 as nf4
+    from paper_2604_02556_b200 import _lib
+
+    torch.cuda.set_device(local_rank)
+    device = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    nf4.load()
+    c = wl.CONFIGS[args.config]
+
+    t_build = time.perf_counter()
+    ws, tensors = build_store(args, rank, world, device)
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t_build
+
+    descs = ws.nf4_tensors()
+    groups = [descs[i:i + _lib.NF4_MAX_BATCH] for i in range(0, len(descs), _lib.NF4_MAX_BATCH)]
+    carrs = [(_lib.TensorDesc * len(g))(*[d.c() for d in g]) for g in groups]
+    lib = nf4.load()
+    odt = _lib.NF4_F16 if c.out_dtype == "f16" else _lib.NF4_BF16
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream or None
+    launch_events = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in carrs]
+
+    def step(timed_launches=None):
+        n_launch = 0
+        for gi, arr in enumerate(carrs):
+            if timed_launches is not None:
+                timed_launches[gi][0].record(stream)
+            st = lib.nf4_dequantize_batched(arr, len(arr), odt, sptr)
+            if st != 0:
+                raise _lib.NF4Error(st, "nf4_dequantize_batched")
+            n_launch += lib.nf4_last_launch_count()
+            if timed_launches is not None:
+                timed_launches[gi][1].record(stream)
+        return n_launch
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # kernel-level roofline pass: CUDA events around every launch, same stream
+    kt = []
+    for _ in range(max(3, min(args.steps, 20))):
+        step(launch_events)
+        torch.cuda.synchronize()
+        kt.append(sum(s.elapsed_time(e) for s, e in launch_events))
+    kernel_ms = statistics.median(kt)
+
+    sampler = ClockSampler(local_rank)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    time.sleep(0.3)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start.record(stream)
+    launches = 0
+    for _ in range(args.steps):
+        launches += step()
+    end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    ms = start.elapsed_time(end)
+    t_max = torch.tensor([ms], dtype=torch.float64, device=device)
+    units = torch.tensor([float(ws.algorithmic_bytes()), float(ws.n_total)], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+        dist.all_reduce(units, op=dist.ReduceOp.SUM)
+    ms_max = float(t_max.item())
+    tot_bytes, tot_elems = float(units[0].item()), float(units[1].item())
+    value = tot_bytes * args.steps / (ms_max * 1e-3) / 1e9
+    gelem = tot_elems * args.steps / (ms_max * 1e-3) / 1e9
+
+    peak, peak_src = _peaks()
+    alg_per_step = ws.algorithmic_bytes()
+    achieved = alg_per_step / (kernel_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                tr = json.load(f)
+            if tr.get("config") == args.config and tr.get("inputs", args.inputs) == args.inputs:
+                traffic = tr.get("traffic_bytes_per_alg_byte")
+                traffic = None if traffic is None else int(traffic * alg_per_step / len(carrs))
+        except Exception:
+            traffic = None
+
+    extra = {}
+    if rank == 0 and not args.no_sol:
+        extra["sol_stream_gbs"] = measure_sol(nf4, torch)
+    e2e = None
+    if not args.no_e2e:
+        try:
+            import psutil
+            avail = psutil.virtual_memory().available
+        except Exception:
+            avail = 16 << 30
+        budget = int(min(avail // (4 * max(world, 1)), args.e2e_host_gb * (1 << 30)))
+        e2e = run_e2e(nf4, torch, ws, args, budget)
+        if world > 1:
+            v = torch.tensor([e2e["value"]], dtype=torch.float64, device=device)
+            dist.all_reduce(v, op=dist.ReduceOp.SUM)  # independent per-rank pipelines; aggregate GB/s
+            e2e["value"] = round(float(v.item()), 2)
+
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu_baseline = time_oracle(args.config, target_s=args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None,
+            "dtype": f"u8->{c.out_dtype}",
+            "data": ("synthetic: W~N(0,0.02^2) per tensor (torch on device), quantized by nf4_quantize"
+                     + (" + nf4_double_quantize" if c.dq else "")) if args.inputs == "gaussian"
+                    else "synthetic: counter-based hash codes/scales (synth.inputs)",
+            "config": {"workload": c.description, "key": args.config,
+                       "model": c.model or "single 4096x4096", "tensors_per_rank": len(tensors),
+                       "elements_per_rank": ws.n_total, "blocksize": c.blocksize,
+                       "absmax": "double-quant" if c.dq else "fp32", "out_dtype": c.out_dtype,
+                       "algorithmic_bytes_per_step_per_rank": alg_per_step,
+                       "launches_per_step": len(carrs),
+                       "l2": "inputs+outputs per step >> 126 MB L2 (no flush needed)"
+                             if alg_per_step > 8 * 126e6 else "L2-resident: reported hot",
+                       "parallelism": f"{args.scaling}-dp{world}" if world > 1 else "single GPU"},
+            "gelem_per_s": round(gelem, 2),
+            "pct_of_peak": {"measured_copy_6551.7": round(100 * value / world / peak, 2),
+                            "nominal_8000": round(100 * value / world / 8000.0, 2)},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": UNIT,
+                         "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "nf4::dequant_kernel", "kernel_ms_per_step": round(kernel_ms, 4),
+                         "bytes_per_step": alg_per_step},
+            "e2e": e2e,
+            "cpu_baseline": cpu_baseline,
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "setup_seconds": round(t_build, 1),
+        }
+        line.update(extra)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="cfg2", choices=sorted(wl.CONFIGS))
+    ap.add_argument("--layers", type=int, default=None, help="limit to the first L decoder layers")
+    ap.add_argument("--inputs", default="gaussian", choices=["gaussian", "hash"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sol", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--ref-step-seconds", type=float, default=5.0)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-host-gb", type=float, default=4.0)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("note: warmup raised to 3 (timing rule)", file=sys.stderr)
+        args.warmup = 3
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

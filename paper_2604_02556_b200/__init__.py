@@ -1,0 +1,196 @@
+"""paper_2604_02556_b200 -- B200-native blockwise NF4 dequantization (arxiv 2604.02556).
+
+Thin Python binding over libnf4.so (C-ABI: include/nf4.h, include/nf4_tools.h).
+Functions carry the C names and only marshal arguments: torch is used for device
+memory and streams; every step of the path runs in the library's sm_100a
+kernels.  There is no CPU fallback: without the built library every call raises.
+
+    import torch, paper_2604_02556_b200 as nf4
+    packed, absmax = nf4.nf4_quantize(w, blocksize=64)            # inputs
+    out = nf4.nf4_dequantize(packed, absmax, n=w.numel(), blocksize=64,
+                             out_dtype=torch.float16)              # the hot path
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+from . import _lib
+from ._lib import NF4Error, load, status_string  # noqa: F401
+
+__all__ = [
+    "DQ", "NF4Tensor", "NF4Error", "load", "status_string",
+    "nf4_dequantize", "nf4_dequantize_batched", "nf4_dequantize_host", "nf4_host_workspace_bytes",
+    "nf4_quantize", "nf4_double_quantize", "nf4_codebook", "nf4_last_launch_count",
+    "nf4_synth_fill", "nf4_sol_stream", "nf4_set_max_ctas", "nf4_dequant_grid", "nf4_dequant_tile_elems",
+]
+
+
+def _ptr(t) -> Optional[int]:
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    if hasattr(t, "data_ptr"):
+        return t.data_ptr() if t.numel() > 0 else None
+    if hasattr(t, "ctypes"):  # numpy
+        return t.ctypes.data if t.size > 0 else None
+    raise TypeError(f"cannot take a pointer of {type(t)}")
+
+
+def _stream(stream) -> Optional[int]:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream or None
+    if isinstance(stream, int):
+        return stream or None
+    return stream.cuda_stream or None
+
+
+def _dtype_code(dt) -> int:
+    import torch
+    if dt in (torch.float16, "f16", "fp16", _lib.NF4_F16):
+        return _lib.NF4_F16
+    if dt in (torch.bfloat16, "bf16", _lib.NF4_BF16):
+        return _lib.NF4_BF16
+    if dt in (torch.float32, "f32", "fp32", _lib.NF4_F32):
+        return _lib.NF4_F32
+    raise ValueError(f"unsupported dtype {dt}")
+
+
+@dataclass
+class DQ:
+    """Double-quantized absmax state (nf4_dq_state): qabsmax uint8[nb], code2
+    fp32[256], absmax2 fp32[ceil(nb/256)], offset, blocksize2 (= 256)."""
+    qabsmax: object
+    code2: object
+    absmax2: object
+    offset: float
+    blocksize2: int = 256
+
+    def c(self) -> _lib.DQState:
+        return _lib.DQState(_ptr(self.qabsmax), _ptr(self.code2), _ptr(self.absmax2),
+                            float(self.offset), int(self.blocksize2))
+
+
+@dataclass
+class NF4Tensor:
+    """One tensor of a batched call (nf4_tensor)."""
+    packed: object
+    n: int
+    blocksize: int
+    out: object
+    absmax: object = None
+    dq: Optional[DQ] = None
+
+    def c(self) -> _lib.TensorDesc:
+        d = _lib.TensorDesc()
+        d.packed = _ptr(self.packed)
+        d.absmax = _ptr(self.absmax)
+        d.dq = self.dq.c() if self.dq is not None else _lib.DQState(None, None, None, 0.0, 256)
+        d.n = int(self.n)
+        d.blocksize = int(self.blocksize)
+        d.reserved = 0
+        d.out = _ptr(self.out)
+        return d
+
+
+def nf4_dequantize(packed, absmax=None, dq: Optional[DQ] = None, *, n: int, blocksize: int = 64,
+                   out_dtype="f16", out=None, stream=None):
+    """out[k] = RNE16(fl32(NF4[code_k] * absmax_b)) for k < n (include/nf4.h).
+    Allocates `out` with torch if not given; returns it."""
+    import torch
+    code = _dtype_code(out_dtype)
+    if out is None:
+        out = torch.empty(n, dtype=torch.float16 if code == _lib.NF4_F16 else torch.bfloat16,
+                          device=packed.device)
+    dqc = dq.c() if dq is not None else None
+    st = load().nf4_dequantize(_ptr(packed), _ptr(absmax), ctypes.byref(dqc) if dqc is not None else None,
+                               int(n), int(blocksize), code, _ptr(out), _stream(stream))
+    _lib.check(st, "nf4_dequantize")
+    return out
+
+
+def nf4_dequantize_batched(tensors: Sequence[NF4Tensor], out_dtype="f16", stream=None) -> None:
+    arr = (_lib.TensorDesc * max(len(tensors), 1))(*[t.c() for t in tensors])
+    st = load().nf4_dequantize_batched(arr, len(tensors), _dtype_code(out_dtype), _stream(stream))
+    _lib.check(st, "nf4_dequantize_batched")
+
+
+def nf4_host_workspace_bytes(chunk_elems: int, blocksize: int, dq: bool) -> int:
+    return int(load().nf4_host_workspace_bytes(int(chunk_elems), int(blocksize), int(bool(dq))))
+
+
+def nf4_dequantize_host(packed, absmax=None, dq: Optional[DQ] = None, *, n: int, blocksize: int = 64,
+                        out_dtype="f16", out, workspace, chunk_elems: int, stream=None) -> None:
+    """Host-buffer end-to-end path: all array arguments are host (ideally pinned)
+    tensors/arrays; `workspace` is a device buffer of nf4_host_workspace_bytes()."""
+    dqc = dq.c() if dq is not None else None
+    nbytes = workspace.numel() * workspace.element_size()
+    st = load().nf4_dequantize_host(_ptr(packed), _ptr(absmax), ctypes.byref(dqc) if dqc is not None else None,
+                                    int(n), int(blocksize), _dtype_code(out_dtype), _ptr(out), _ptr(workspace),
+                                    int(nbytes), int(chunk_elems), _stream(stream))
+    _lib.check(st, "nf4_dequantize_host")
+
+
+def nf4_quantize(x, blocksize: int = 64, packed=None, absmax=None, stream=None):
+    """GPU NF4 quantizer (input generator).  x: CUDA tensor f32/f16/bf16.
+    Returns (packed uint8[ceil(n/2)], absmax fp32[ceil(n/blocksize)])."""
+    import torch
+    n = x.numel()
+    if packed is None:
+        packed = torch.empty((n + 1) // 2, dtype=torch.uint8, device=x.device)
+    if absmax is None:
+        absmax = torch.empty(-(-n // blocksize), dtype=torch.float32, device=x.device)
+    st = load().nf4_quantize(_ptr(x), _dtype_code(x.dtype), n, int(blocksize), _ptr(packed), _ptr(absmax),
+                             _stream(stream))
+    _lib.check(st, "nf4_quantize")
+    return packed, absmax
+
+
+def nf4_double_quantize(absmax, offset: float, code2, qabsmax=None, absmax2=None, blocksize2: int = 256,
+                        stream=None) -> DQ:
+    """GPU second-level quantizer (input generator).  Returns the DQ state."""
+    import torch
+    nb = absmax.numel()
+    if qabsmax is None:
+        qabsmax = torch.empty(nb, dtype=torch.uint8, device=absmax.device)
+    if absmax2 is None:
+        absmax2 = torch.empty(-(-nb // blocksize2), dtype=torch.float32, device=absmax.device)
+    st = load().nf4_double_quantize(_ptr(absmax), nb, float(offset), _ptr(code2), int(blocksize2), _ptr(qabsmax),
+                                    _ptr(absmax2), _stream(stream))
+    _lib.check(st, "nf4_double_quantize")
+    return DQ(qabsmax, code2, absmax2, float(offset), blocksize2)
+
+
+def nf4_codebook():
+    buf = (ctypes.c_float * 16)()
+    load().nf4_codebook(buf)
+    return list(buf)
+
+
+def nf4_last_launch_count() -> int:
+    return int(load().nf4_last_launch_count())
+
+
+def nf4_synth_fill(kind: int, seed: int, begin: int, count: int, dst, stream=None) -> None:
+    st = load().nf4_synth_fill(int(kind), int(seed), int(begin), int(count), _ptr(dst), _stream(stream))
+    _lib.check(st, "nf4_synth_fill")
+
+
+def nf4_sol_stream(src, in_bytes: int, dst, stream=None) -> None:
+    st = load().nf4_sol_stream(_ptr(src), int(in_bytes), _ptr(dst), _stream(stream))
+    _lib.check(st, "nf4_sol_stream")
+
+
+def nf4_set_max_ctas(max_ctas: int) -> None:
+    load().nf4_set_max_ctas(int(max_ctas))
+
+
+def nf4_dequant_grid(tiles: int) -> int:
+    return int(load().nf4_dequant_grid(int(tiles)))
+
+
+def nf4_dequant_tile_elems() -> int:
+    return int(load().nf4_dequant_tile_elems())

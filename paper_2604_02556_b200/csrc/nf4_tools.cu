@@ -1,0 +1,259 @@
+// nf4_tools.cu -- input generation (counter-based hash, same function as
+// synth/inputs.py), the speed-of-light stream kernel, and the host-buffer
+// (end-to-end) dequantization pipeline.  None of this is the method's
+// arithmetic except nf4_dequantize_host, which only moves bytes around calls
+// of the device kernel in nf4_dequant.cu.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "nf4_internal.cuh"
+
+namespace nf4 {
+
+// ---------------------------------------------------------------------------
+// Counter-based generator: z = splitmix64_mix(seed*GOLDEN + stream*MUL + idx)
+// (synth/inputs.py hash64).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t synth_hash(uint64_t seed, uint64_t stream, uint64_t idx) {
+  uint64_t z = seed * 0x9E3779B97F4A7C15ull + stream * 0xD1B54A32D192ED03ull + idx;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void synth_bytes_kernel(uint64_t seed, uint64_t stream, int64_t begin, int64_t count, uint8_t* dst) {
+  const int64_t w0 = begin >> 3;
+  const int64_t w1 = (begin + count + 7) >> 3;
+  const bool fast = ((begin & 7) == 0) && ((reinterpret_cast<uintptr_t>(dst) & 7) == 0);
+  for (int64_t w = w0 + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; w < w1;
+       w += int64_t(gridDim.x) * blockDim.x) {
+    const uint64_t z = synth_hash(seed, stream, uint64_t(w));
+    const int64_t j0 = w << 3;
+    if (fast && j0 + 8 <= begin + count) {
+      *reinterpret_cast<uint64_t*>(dst + (j0 - begin)) = z;  // little-endian bytes
+    } else {
+      for (int i = 0; i < 8; ++i) {
+        const int64_t j = j0 + i;
+        if (j >= begin && j < begin + count) dst[j - begin] = uint8_t(z >> (8 * i));
+      }
+    }
+  }
+}
+
+__global__ void synth_f32_kernel(uint64_t seed, uint64_t stream, int64_t begin, int64_t count, uint32_t base,
+                                 uint32_t mask, uint32_t* dst) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x) {
+    const uint64_t z = synth_hash(seed, stream, uint64_t(begin + i));
+    dst[i] = base | (uint32_t(z) & mask);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Speed-of-light stream with the dequant kernel's exact access pattern:
+// per thread and tile, 4 x 8-byte loads (warp-contiguous 256 B) and
+// 4 x 32-byte evict-first stores (warp-contiguous 1 KB); no table, no math.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) sol_stream_kernel(const uint8_t* __restrict__ src, int64_t in_bytes,
+                                                         uint8_t* __restrict__ dst) {
+  const int64_t tiles = in_bytes / 8192;  // 8 KB of input per tile (= 16384 elements)
+  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    uint2 q[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) q[u] = ld_codes_v2(src + t * 8192 + (u * 256 + threadIdx.x) * 8);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      uint32_t w[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) w[j] = (j < 4 ? q[u].x : q[u].y) * 0x00010001u;
+      st_out_v8(dst + (t * 8192 + (u * 256 + threadIdx.x) * 8) * 4, w);
+    }
+  }
+}
+
+}  // namespace nf4
+
+using namespace nf4;
+
+extern "C" nf4_status nf4_synth_fill(nf4_synth_kind kind, uint64_t seed, int64_t begin, int64_t count, void* dst,
+                                     void* stream) {
+  if (count < 0 || begin < 0) return NF4_ERR_BAD_SIZE;
+  if (count == 0) { set_launch_count(0); return NF4_OK; }
+  if (!dst) return NF4_ERR_NULL_POINTER;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int grid = sm_count() * 8;
+  switch (kind) {
+    case NF4_SYNTH_CODES:
+    case NF4_SYNTH_QABSMAX:
+      synth_bytes_kernel<<<grid, 256, 0, s>>>(seed, uint64_t(kind), begin, count, static_cast<uint8_t*>(dst));
+      break;
+    case NF4_SYNTH_ABSMAX:
+      if (!aligned(dst, 4)) return NF4_ERR_MISALIGNED;
+      synth_f32_kernel<<<grid, 256, 0, s>>>(seed, uint64_t(kind), begin, count, 0x3D000000u, 0x7FFFFFu,
+                                            static_cast<uint32_t*>(dst));
+      break;
+    case NF4_SYNTH_ABSMAX2:
+      if (!aligned(dst, 4)) return NF4_ERR_MISALIGNED;
+      synth_f32_kernel<<<grid, 256, 0, s>>>(seed, uint64_t(kind), begin, count, 0x3C800000u, 0x7FFFFFu,
+                                            static_cast<uint32_t*>(dst));
+      break;
+    default:
+      return NF4_ERR_BAD_DTYPE;
+  }
+  if (cudaPeekAtLastError() != cudaSuccess) { cudaGetLastError(); return NF4_ERR_CUDA; }
+  set_launch_count(1);
+  return NF4_OK;
+}
+
+extern "C" nf4_status nf4_sol_stream(const void* src, int64_t in_bytes, void* dst, void* stream) {
+  if (in_bytes < 0 || in_bytes % 8192 != 0) return NF4_ERR_BAD_SIZE;
+  if (in_bytes == 0) { set_launch_count(0); return NF4_OK; }
+  if (!src || !dst) return NF4_ERR_NULL_POINTER;
+  if (!aligned(src, 32) || !aligned(dst, 128)) return NF4_ERR_MISALIGNED;
+  static int occ = 0;
+  if (occ == 0) {
+    int v = 0;
+    occ = (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, sol_stream_kernel, 256, 0) == cudaSuccess && v > 0)
+              ? v : 4;
+  }
+  int64_t grid = int64_t(sm_count()) * occ;
+  const int32_t cap = max_ctas();
+  if (cap > 0 && grid > cap) grid = cap;
+  const int64_t tiles = in_bytes / 8192;
+  if (grid > tiles) grid = tiles;
+  sol_stream_kernel<<<int(grid), 256, 0, (cudaStream_t)stream>>>(static_cast<const uint8_t*>(src), in_bytes,
+                                                                 static_cast<uint8_t*>(dst));
+  if (cudaPeekAtLastError() != cudaSuccess) { cudaGetLastError(); return NF4_ERR_CUDA; }
+  set_launch_count(1);
+  return NF4_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Host-buffer pipeline (nf4_dequantize_host)
+// ---------------------------------------------------------------------------
+namespace {
+struct HostLayout {
+  int64_t codes, scales, groups, out, slot;  // byte sizes (256-B rounded)
+};
+inline int64_t rnd(int64_t v) { return (v + 255) / 256 * 256; }
+HostLayout host_layout(int64_t chunk, int32_t bs, bool dq) {
+  HostLayout L;
+  const int64_t nb = chunk / bs;
+  L.codes = rnd(chunk / 2);
+  L.scales = rnd(dq ? nb : nb * 4);
+  L.groups = dq ? rnd((nb / 256) * 4) : 0;
+  L.out = rnd(chunk * 2);
+  L.slot = L.codes + L.scales + L.groups + L.out;
+  return L;
+}
+}  // namespace
+
+extern "C" int64_t nf4_host_workspace_bytes(int64_t chunk_elems, int32_t blocksize, int32_t dq) {
+  if (chunk_elems <= 0 || !is_pow2(blocksize)) return 0;
+  const HostLayout L = host_layout(chunk_elems, blocksize, dq != 0);
+  return 2 * L.slot + (dq ? 1024 : 0);
+}
+
+extern "C" nf4_status nf4_dequantize_host(const uint8_t* packed, const float* absmax, const nf4_dq_state* dq,
+                                          int64_t n, int32_t blocksize, nf4_dtype out_dtype, void* out,
+                                          void* workspace, int64_t workspace_bytes, int64_t chunk_elems,
+                                          void* stream) {
+  if (n < 0) return NF4_ERR_BAD_SIZE;
+  if (!is_pow2(blocksize) || blocksize < 64 || blocksize > 4096) return NF4_ERR_BAD_BLOCKSIZE;
+  if (out_dtype != NF4_F16 && out_dtype != NF4_BF16) return NF4_ERR_BAD_DTYPE;
+  if ((absmax == nullptr) == (dq == nullptr)) return NF4_ERR_BAD_STATE;
+  if (dq && dq->blocksize2 != 256) return NF4_ERR_BAD_STATE;
+  if (n == 0) { set_launch_count(0); return NF4_OK; }
+  if (!packed || !out || !workspace) return NF4_ERR_NULL_POINTER;
+  if (dq && (!dq->qabsmax || !dq->code2 || !dq->absmax2)) return NF4_ERR_NULL_POINTER;
+  if (chunk_elems <= 0 || chunk_elems % (int64_t(256) * blocksize) != 0) return NF4_ERR_BAD_SIZE;
+  if (!aligned(workspace, 256)) return NF4_ERR_MISALIGNED;
+  const bool isdq = dq != nullptr;
+  if (workspace_bytes < nf4_host_workspace_bytes(chunk_elems, blocksize, isdq)) return NF4_ERR_BAD_STATE;
+
+  const HostLayout L = host_layout(chunk_elems, blocksize, isdq);
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  float* d_code2 = isdq ? reinterpret_cast<float*>(ws + 2 * L.slot) : nullptr;
+  cudaStream_t cs = (cudaStream_t)stream;
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
+  nf4_status st = NF4_OK;
+  int32_t launches = 0;
+#define NF4_TRY(x)                       \
+  do {                                   \
+    if ((x) != cudaSuccess) {            \
+      st = NF4_ERR_CUDA;                 \
+      goto done;                         \
+    }                                    \
+  } while (0)
+  NF4_TRY(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
+  NF4_TRY(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i) {
+    NF4_TRY(cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming));
+    NF4_TRY(cudaEventCreateWithFlags(&ev_comp[i], cudaEventDisableTiming));
+    NF4_TRY(cudaEventCreateWithFlags(&ev_out[i], cudaEventDisableTiming));
+  }
+  // h2d must start after everything already queued on the caller's stream
+  NF4_TRY(cudaEventRecord(ev_comp[0], cs));
+  NF4_TRY(cudaStreamWaitEvent(h2d, ev_comp[0], 0));
+  if (isdq) NF4_TRY(cudaMemcpyAsync(d_code2, dq->code2, 1024, cudaMemcpyHostToDevice, h2d));
+  {
+    const int64_t nchunks = (n + chunk_elems - 1) / chunk_elems;
+    for (int64_t c = 0; c < nchunks; ++c) {
+      const int s = int(c & 1);
+      uint8_t* base = ws + s * L.slot;
+      uint8_t* d_codes = base;
+      uint8_t* d_scales = base + L.codes;
+      float* d_groups = reinterpret_cast<float*>(base + L.codes + L.scales);
+      void* d_out = base + L.codes + L.scales + L.groups;
+      const int64_t e0 = c * chunk_elems;
+      const int64_t e1 = (e0 + chunk_elems < n) ? e0 + chunk_elems : n;
+      const int64_t m = e1 - e0;
+      const int64_t b0 = e0 / blocksize, b1 = (e1 + blocksize - 1) / blocksize;
+      if (c >= 2) NF4_TRY(cudaStreamWaitEvent(h2d, ev_comp[s], 0));  // inputs of chunk c-2 consumed
+      NF4_TRY(cudaMemcpyAsync(d_codes, packed + e0 / 2, (m + 1) / 2, cudaMemcpyHostToDevice, h2d));
+      if (isdq) {
+        const int64_t g0 = b0 / 256, g1 = (b1 + 255) / 256;
+        NF4_TRY(cudaMemcpyAsync(d_scales, dq->qabsmax + b0, b1 - b0, cudaMemcpyHostToDevice, h2d));
+        NF4_TRY(cudaMemcpyAsync(d_groups, dq->absmax2 + g0, (g1 - g0) * 4, cudaMemcpyHostToDevice, h2d));
+      } else {
+        NF4_TRY(cudaMemcpyAsync(d_scales, absmax + b0, (b1 - b0) * 4, cudaMemcpyHostToDevice, h2d));
+      }
+      NF4_TRY(cudaEventRecord(ev_in[s], h2d));
+      NF4_TRY(cudaStreamWaitEvent(cs, ev_in[s], 0));
+      if (c >= 2) NF4_TRY(cudaStreamWaitEvent(cs, ev_out[s], 0));  // output slot drained
+      nf4_status ks;
+      if (isdq) {
+        nf4_dq_state ld;
+        ld.qabsmax = d_scales;
+        ld.code2 = d_code2;
+        ld.absmax2 = d_groups;
+        ld.offset = dq->offset;
+        ld.blocksize2 = 256;
+        ks = nf4_dequantize(d_codes, nullptr, &ld, m, blocksize, out_dtype, d_out, cs);
+      } else {
+        ks = nf4_dequantize(d_codes, reinterpret_cast<const float*>(d_scales), nullptr, m, blocksize, out_dtype,
+                            d_out, cs);
+      }
+      if (ks != NF4_OK) { st = ks; goto done; }
+      launches += nf4_last_launch_count();
+      NF4_TRY(cudaEventRecord(ev_comp[s], cs));
+      NF4_TRY(cudaStreamWaitEvent(d2h, ev_comp[s], 0));
+      NF4_TRY(cudaMemcpyAsync(static_cast<uint8_t*>(out) + e0 * 2, d_out, m * 2, cudaMemcpyDeviceToHost, d2h));
+      NF4_TRY(cudaEventRecord(ev_out[s], d2h));
+    }
+  }
+  NF4_TRY(cudaStreamSynchronize(d2h));
+  NF4_TRY(cudaStreamSynchronize(h2d));
+  NF4_TRY(cudaStreamSynchronize(cs));
+done:
+#undef NF4_TRY
+  for (int i = 0; i < 2; ++i) {
+    if (ev_in[i]) cudaEventDestroy(ev_in[i]);
+    if (ev_comp[i]) cudaEventDestroy(ev_comp[i]);
+    if (ev_out[i]) cudaEventDestroy(ev_out[i]);
+  }
+  if (h2d) { cudaStreamSynchronize(h2d); cudaStreamDestroy(h2d); }
+  if (d2h) { cudaStreamSynchronize(d2h); cudaStreamDestroy(d2h); }
+  if (st == NF4_OK) set_launch_count(launches);
+  return st;
+}
