@@ -291,6 +291,9 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist.init_process_group("nccl", device_id=device)
     nf4.load()
+    if args.variant is not None:
+        nf4.nf4_set_kernel_variant(int(args.variant) if args.variant.isdigit() else args.variant)
+    variant = nf4.nf4_kernel_variants()[nf4.nf4_get_kernel_variant()]
     c = wl.CONFIGS[args.config]
 
     t_build = time.perf_counter()
@@ -412,7 +415,7 @@ def run_ours(args, rank, world, local_rank):
                        "elements_per_rank": ws.n_total, "blocksize": c.blocksize,
                        "absmax": "double-quant" if c.dq else "fp32", "out_dtype": c.out_dtype,
                        "algorithmic_bytes_per_step_per_rank": alg_per_step,
-                       "launches_per_step": len(carrs),
+                       "launches_per_step": len(carrs), "kernel_variant": variant,
                        "l2": "inputs+outputs per step >> 126 MB L2 (no flush needed)"
                              if alg_per_step > 8 * 126e6 else "L2-resident: reported hot",
                        "parallelism": f"{args.scaling}-dp{world}" if world > 1 else "single GPU"},
@@ -445,6 +448,7 @@ def main():
     ap.add_argument("--inputs", default="gaussian", choices=["gaussian", "hash"])
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--variant", default=None, help="dequant kernel variant (name or index)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sol", action="store_true")

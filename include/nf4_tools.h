@@ -31,13 +31,25 @@ nf4_status nf4_synth_fill(nf4_synth_kind kind, uint64_t seed, int64_t begin, int
                           void* dst, void* stream);
 
 /* Speed-of-light stream: reads in_bytes from src, writes 4*in_bytes to dst
- * (dst[i] = byte i/4 of src replicated), 256-bit accesses, persistent grid.
- * in_bytes must be a multiple of 32, src 32-byte and dst 128-byte aligned. */
+ * with the default dequant variant's access pattern (16-byte loads, 2 x 32-byte
+ * stores per thread-group, one CTA per 8 KB input tile) and no arithmetic:
+ * every 32-bit input word w becomes four output words w * 0x00010001.
+ * in_bytes must be a multiple of 8192, src 32-byte and dst 128-byte aligned. */
 nf4_status nf4_sol_stream(const void* src, int64_t in_bytes, void* dst, void* stream);
 
 /* Cap the persistent grid of every following launch at max_ctas CTAs
  * (0 = automatic: SM count x resident CTAs per SM).  Process-wide. */
 void nf4_set_max_ctas(int32_t max_ctas);
+
+/* Dequant kernel variants (all bit-identical).
+ * The default is the fastest measured variant unless NF4_KERNEL_VARIANT
+ * names another one (by name or index).
+ * nf4_set_kernel_variant returns the variant in effect afterwards (an
+ * out-of-range request leaves it unchanged).  Process-wide. */
+int32_t nf4_kernel_variant_count(void);
+const char* nf4_kernel_variant_name(int32_t variant);
+int32_t nf4_set_kernel_variant(int32_t variant);
+int32_t nf4_get_kernel_variant(void);
 
 /* Grid size (CTAs) the next dequantize launch on the current device would use
  * for `tiles` work tiles, and the number of elements per tile. */

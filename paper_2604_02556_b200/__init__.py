@@ -24,6 +24,7 @@ __all__ = [
     "nf4_dequantize", "nf4_dequantize_batched", "nf4_dequantize_host", "nf4_host_workspace_bytes",
     "nf4_quantize", "nf4_double_quantize", "nf4_codebook", "nf4_last_launch_count",
     "nf4_synth_fill", "nf4_sol_stream", "nf4_set_max_ctas", "nf4_dequant_grid", "nf4_dequant_tile_elems",
+    "nf4_kernel_variants", "nf4_set_kernel_variant", "nf4_get_kernel_variant",
 ]
 
 
@@ -194,3 +195,19 @@ def nf4_dequant_grid(tiles: int) -> int:
 
 def nf4_dequant_tile_elems() -> int:
     return int(load().nf4_dequant_tile_elems())
+
+
+def nf4_kernel_variants():
+    lib = load()
+    return [lib.nf4_kernel_variant_name(i).decode() for i in range(lib.nf4_kernel_variant_count())]
+
+
+def nf4_set_kernel_variant(v) -> int:
+    """Select the dequant kernel variant by index or name; returns the one in effect."""
+    if isinstance(v, str):
+        v = nf4_kernel_variants().index(v)
+    return int(load().nf4_set_kernel_variant(int(v)))
+
+
+def nf4_get_kernel_variant() -> int:
+    return int(load().nf4_get_kernel_variant())

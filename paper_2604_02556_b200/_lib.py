@@ -23,6 +23,7 @@ EXPORTS = [
     "nf4_dequantize", "nf4_dequantize_batched", "nf4_dequantize_host", "nf4_host_workspace_bytes",
     "nf4_quantize", "nf4_double_quantize", "nf4_codebook", "nf4_status_string", "nf4_last_launch_count",
     "nf4_synth_fill", "nf4_sol_stream", "nf4_set_max_ctas", "nf4_dequant_grid", "nf4_dequant_tile_elems",
+    "nf4_kernel_variant_count", "nf4_kernel_variant_name", "nf4_set_kernel_variant", "nf4_get_kernel_variant",
 ]
 
 
@@ -75,6 +76,10 @@ def load() -> ctypes.CDLL:
             "nf4_set_max_ctas": ([i32], None),
             "nf4_dequant_grid": ([i64], i32),
             "nf4_dequant_tile_elems": ([], i64),
+            "nf4_kernel_variant_count": ([], i32),
+            "nf4_kernel_variant_name": ([i32], ctypes.c_char_p),
+            "nf4_set_kernel_variant": ([i32], i32),
+            "nf4_get_kernel_variant": ([], i32),
         }
         for name, (args, res) in sig.items():
             fn = getattr(lib, name)

@@ -21,6 +21,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -28,10 +30,45 @@
 
 namespace nf4 {
 
-constexpr int kThreads = 256;           // 8 warps per CTA
-constexpr int kGroup = 16;              // elements per thread-group (8 code bytes, 32 B out)
-constexpr int kUnroll = 4;              // groups per thread per tile
-constexpr int64_t kTile = int64_t(kThreads) * kGroup * kUnroll;  // 16384 elements
+constexpr int kThreads = 256;  // 8 warps per CTA
+
+// Kernel variants (A/B-able at run time through NF4_KERNEL_VARIANT or
+// nf4_set_kernel_variant; all are bit-identical -- tests/test_parity_gpu.py).
+//   vec     code bytes per thread-group: 8 (LDG.64, 16 elements, one STG.256)
+//           or 16 (LDG.128, 32 elements, two STG.256 = 64 B thread-contiguous)
+//   unroll  thread-groups per thread per tile (all loads issued first)
+//   persist grid = SMs x resident CTAs striding over tiles, instead of one CTA
+//           per tile (the block scheduler then keeps the DRAM working set of
+//           concurrently running CTAs compact: +13% measured on B200)
+//   sscale  the tile's block scales are decoded once per block into shared
+//           memory (one thread per block) instead of once per thread-group
+//   prmt    nibble -> LUT byte offset for 4 bytes at once with SHF+LOP3, then
+//           one PRMT per element (1.5 instead of ~2.2 ALU ops per element)
+//   clc     Blackwell cluster launch control: a running CTA cancels a not yet
+//           launched CTA (clusterlaunchcontrol.try_cancel) and takes its tile,
+//           so the prologue (LUT staging, descriptor search) is paid once per
+//           CTA while tiles are still handed out in launch order
+struct Variant {
+  const char* name;
+  int vec, unroll;
+  bool persist, sscale, prmt, clc;
+};
+static const Variant kVariants[] = {
+    {"v2u4", 8, 4, false, false, false, false},      // 0
+    {"v4u2", 16, 2, false, false, false, false},     // 1
+    {"v4u4", 16, 4, false, false, false, false},     // 2
+    {"v2u4p", 8, 4, true, false, false, false},      // 3 (round-1 first version)
+    {"v4u1", 16, 1, false, false, false, false},     // 4
+    {"v2u8", 8, 8, false, false, false, false},      // 5
+    {"v2u4s", 8, 4, false, true, false, false},      // 6
+    {"v2u4sx", 8, 4, false, true, true, false},      // 7
+    {"v2u4sxc", 8, 4, false, true, true, true},      // 8
+    {"v2u4c", 8, 4, false, false, false, true},      // 9
+    {"v2u4xc", 8, 4, false, false, true, true},      // 10
+};
+constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
+constexpr int kDefaultVariant = 8;   // v2u4sxc: best measured on B200 (profiles/r01_variants.md)
+constexpr int kMaxTileBlocks = 256;  // TILE / 64 for the 16384-element tiles using sscale
 
 struct TensorDesc {
   const uint8_t* packed;
@@ -44,7 +81,7 @@ struct TensorDesc {
   int64_t tile_end;       // exclusive prefix of tiles over the batch
   float offset;
   int32_t bs_shift;       // log2(blocksize)
-  int32_t vec_ok;         // packed 8-B aligned and out 32-B aligned
+  int32_t vec_ok;         // packed VEC-B aligned and out 32-B aligned
   int32_t pad_;
 };
 
@@ -65,25 +102,73 @@ __device__ __forceinline__ float block_scale(const TensorDesc& d, int64_t b) {
   return __fadd_rn(__fmul_rn(c, s2), d.offset);
 }
 
-// 16 elements from 8 code bytes: element 2j <- high nibble of byte j.
-template <bool BF16>
-__device__ __forceinline__ void decode16(const float* lut, uint2 q, float a, uint32_t (&w)[8]) {
+template <int VEC>
+struct CodeVec {
+  uint32_t w[VEC / 4];
+};
+
+template <int VEC>
+__device__ __forceinline__ CodeVec<VEC> ld_codes(const uint8_t* p) {
+  CodeVec<VEC> r;
+  if constexpr (VEC == 8) {
+    asm("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(r.w[0]), "=r"(r.w[1]) : "l"(p));
+  } else {
+    asm("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+        : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3])
+        : "l"(p));
+  }
+  return r;
+}
+
+__device__ __forceinline__ float lut_at(const float* lut, uint32_t byte_off) {
+  return *reinterpret_cast<const float*>(reinterpret_cast<const char*>(lut) + byte_off);
+}
+
+// 2*VEC elements from VEC code bytes: element 2j <- high nibble of byte j
+// (P:160-161), product fl32(NF4[idx] * a), RNE to 16 bits;
+// word j holds elements (2j, 2j+1) with 2j in the low half.
+template <bool BF16, int VEC, bool PRMT>
+__device__ __forceinline__ void decode_group(const float* lut, const CodeVec<VEC>& q, float a,
+                                             uint32_t (&w)[VEC]) {
+  if constexpr (PRMT) {
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const uint32_t word = j < 4 ? q.x : q.y;
-    const uint32_t byte = (word >> (8 * (j & 3))) & 0xFFu;
-    const float ph = __fmul_rn(lut[byte >> 4], a);    // element 2j
-    const float pl = __fmul_rn(lut[byte & 0x0Fu], a); // element 2j+1
-    w[j] = pack2_rn<BF16>(ph, pl);
+    for (int i = 0; i < VEC / 4; ++i) {
+      const uint32_t x = q.w[i];
+      const uint32_t hi4 = (x >> 2) & 0x3C3C3C3Cu;  // byte k = 4 * (high nibble of byte k)
+      const uint32_t lo4 = (x << 2) & 0x3C3C3C3Cu;  // byte k = 4 * (low nibble of byte k)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t oh = k == 0 ? (hi4 & 0xFFu) : k == 3 ? (hi4 >> 24) : __byte_perm(hi4, 0u, 0x4440u + k);
+        const uint32_t ol = k == 0 ? (lo4 & 0xFFu) : k == 3 ? (lo4 >> 24) : __byte_perm(lo4, 0u, 0x4440u + k);
+        const float ph = __fmul_rn(lut_at(lut, oh), a);  // element 2j
+        const float pl = __fmul_rn(lut_at(lut, ol), a);  // element 2j+1
+        w[4 * i + k] = pack2_rn<BF16>(ph, pl);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) {
+      const uint32_t byte = (q.w[j >> 2] >> (8 * (j & 3))) & 0xFFu;
+      const float ph = __fmul_rn(lut[byte >> 4], a);     // element 2j
+      const float pl = __fmul_rn(lut[byte & 0x0Fu], a);  // element 2j+1
+      w[j] = pack2_rn<BF16>(ph, pl);
+    }
+  }
+}
+
+template <int VEC>
+__device__ __forceinline__ void st_group(uint16_t* out, const uint32_t (&w)[VEC]) {
+#pragma unroll
+  for (int h = 0; h < VEC / 8; ++h) {
+    const uint32_t(&ww)[8] = *reinterpret_cast<const uint32_t(*)[8]>(&w[8 * h]);
+    st_out_v8(out + 16 * h, ww);
   }
 }
 
 // Element-wise path for tails and unaligned tensors.
-template <bool BF16>
-__device__ __forceinline__ void slow_group(const TensorDesc& d, const float* lut, int64_t e0) {
-  const int64_t e1 = e0 + kGroup < d.n ? e0 + kGroup : d.n;
-  if (e0 >= e1) return;
-  const float a = block_scale(d, e0 >> d.bs_shift);  // 16 | blocksize: one block per group
+template <bool BF16, int GROUP>
+__device__ __forceinline__ void slow_group(const TensorDesc& d, const float* lut, int64_t e0, float a) {
+  const int64_t e1 = e0 + GROUP < d.n ? e0 + GROUP : d.n;
   for (int64_t k = e0; k < e1; ++k) {
     const uint32_t byte = d.packed[k >> 1];
     const uint32_t idx = (k & 1) ? (byte & 0x0Fu) : (byte >> 4);
@@ -91,77 +176,198 @@ __device__ __forceinline__ void slow_group(const TensorDesc& d, const float* lut
   }
 }
 
-template <bool BF16>
+// --- cluster launch control (sm_100) ---------------------------------------
+__device__ __forceinline__ void clc_try_cancel(void* result, uint64_t* bar) {
+  const uint32_t r = static_cast<uint32_t>(__cvta_generic_to_shared(result));
+  const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+  asm volatile("fence.proxy.async::generic.acquire.sync_restrict::shared::cluster.cluster;" ::: "memory");
+  asm volatile("clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.b128 [%0], [%1];"
+               ::"r"(r), "r"(b) : "memory");
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], 16;" ::"r"(b) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, p;\n\t}"
+        : "=r"(done) : "r"(b), "r"(phase) : "memory");
+  }
+}
+
+// Returns the canceled CTA's blockIdx.x, or -1 if no CTA was canceled.
+__device__ __forceinline__ int64_t clc_result(const uint4* result) {
+  const volatile uint32_t* rv = reinterpret_cast<const volatile uint32_t*>(result);
+  const uint4 r = make_uint4(rv[0], rv[1], rv[2], rv[3]);
+  uint32_t ok, x;
+  asm volatile(
+      "{\n\t.reg .b128 h;\n\t.reg .pred p;\n\t"
+      "mov.b128 h, {%2, %3};\n\t"
+      "clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 p, h;\n\t"
+      "selp.b32 %0, 1, 0, p;\n\t"
+      "clusterlaunchcontrol.query_cancel.get_first_ctaid::x.b32.b128 %1, h;\n\t}"
+      : "=r"(ok), "=r"(x)
+      : "l"((uint64_t(r.y) << 32) | r.x), "l"((uint64_t(r.w) << 32) | r.z));
+  asm volatile("fence.proxy.async::generic.release.sync_restrict::shared::cta.cluster;" ::: "memory");
+  return ok ? int64_t(x) : -1;
+}
+
+template <bool BF16, int VEC, int U, bool PERSIST, bool SSCALE, bool PRMT, bool CLC>
 __global__ void __launch_bounds__(kThreads) dequant_kernel(const __grid_constant__ BatchParams P) {
+  constexpr int GROUP = 2 * VEC;                      // elements per thread-group
+  constexpr int64_t TILE = int64_t(kThreads) * GROUP * U;
+  static_assert(!SSCALE || TILE / 64 <= kMaxTileBlocks, "tile too large for the scale cache");
+  // A1: stage the 16-entry table in shared memory (16 banks, conflict-free).
   __shared__ float lut[16];
+  __shared__ float sscale[SSCALE ? kMaxTileBlocks : 1];
+  __shared__ __align__(16) uint4 clc_res;
+  __shared__ __align__(8) uint64_t clc_bar;
   if (threadIdx.x < 16) lut[threadIdx.x] = __uint_as_float(c_nf4_bits[threadIdx.x]);
+  if (CLC && threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+        static_cast<uint32_t>(__cvta_generic_to_shared(&clc_bar))) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();
 
   int cur = 0;
-  for (int64_t tile = blockIdx.x; tile < P.total_tiles; tile += gridDim.x) {
-    while (tile >= P.t[cur].tile_end) ++cur;
-    const TensorDesc& d = P.t[cur];
-    const int64_t first = cur == 0 ? 0 : P.t[cur - 1].tile_end;
-    const int64_t e_tile = (tile - first) * kTile;
+  uint32_t phase = 0;
+  int64_t cta = blockIdx.x;  // CTA id whose tiles we process (own, then stolen ones)
+  while (true) {
+    if (CLC && threadIdx.x == 0) clc_try_cancel(&clc_res, &clc_bar);
+    for (int64_t tile = cta; tile < P.total_tiles; tile += gridDim.x) {
+      if (PERSIST || CLC) {  // tiles arrive (mostly) in increasing order: walk a cursor
+        while (tile >= P.t[cur].tile_end) ++cur;
+        while (cur > 0 && tile < P.t[cur - 1].tile_end) --cur;
+      } else {  // first tensor whose tile range contains `tile` (binary search, <= 7 steps)
+        int lo = 0, hi = P.count - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (tile < P.t[mid].tile_end) hi = mid; else lo = mid + 1;
+        }
+        cur = lo;
+      }
+      const TensorDesc& d = P.t[cur];
+      const int64_t first = cur == 0 ? 0 : P.t[cur - 1].tile_end;
+      const int64_t e_tile = (tile - first) * TILE;
+      const bool full = d.vec_ok && e_tile + TILE <= d.n;
 
-    if (d.vec_ok && e_tile + kTile <= d.n) {
-      uint2 q[kUnroll];
-      float a[kUnroll];
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const int64_t e0 = e_tile + int64_t(u * kThreads + threadIdx.x) * kGroup;
-        q[u] = ld_codes_v2(d.packed + (e0 >> 1));
+      if (SSCALE) {
+        // A4 once per quantization block of this tile (one thread per block)
+        const int64_t b0 = e_tile >> d.bs_shift;
+        const int64_t nb = (d.n + (int64_t(1) << d.bs_shift) - 1) >> d.bs_shift;
+        const int nblk = int(((TILE - 1) >> d.bs_shift) + 1);
+        if (int(threadIdx.x) < nblk && b0 + threadIdx.x < nb) sscale[threadIdx.x] = block_scale(d, b0 + threadIdx.x);
+        __syncthreads();
       }
+      auto scale_of = [&](int64_t e0) -> float {
+        return SSCALE ? sscale[(e0 - e_tile) >> d.bs_shift] : block_scale(d, e0 >> d.bs_shift);
+      };
+
+      if (full) {
+        CodeVec<VEC> q[U];
+        float a[U];
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const int64_t e0 = e_tile + int64_t(u * kThreads + threadIdx.x) * kGroup;
-        a[u] = block_scale(d, e0 >> d.bs_shift);
-      }
+        for (int u = 0; u < U; ++u) {
+          const int64_t e0 = e_tile + int64_t(u * kThreads + threadIdx.x) * GROUP;
+          q[u] = ld_codes<VEC>(d.packed + (e0 >> 1));
+        }
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const int64_t e0 = e_tile + int64_t(u * kThreads + threadIdx.x) * kGroup;
-        uint32_t w[8];
-        decode16<BF16>(lut, q[u], a[u], w);
-        st_out_v8(d.out + e0, w);
-      }
-    } else {
-      for (int u = 0; u < kUnroll; ++u) {
-        const int64_t e0 = e_tile + int64_t(u * kThreads + threadIdx.x) * kGroup;
-        if (e0 >= d.n) break;
-        if (d.vec_ok && e0 + kGroup <= d.n) {
-          uint32_t w[8];
-          decode16<BF16>(lut, ld_codes_v2(d.packed + (e0 >> 1)), block_scale(d, e0 >> d.bs_shift), w);
-          st_out_v8(d.out + e0, w);
-        } else {
-          slow_group<BF16>(d, lut, e0);
+        for (int u = 0; u < U; ++u) a[u] = scale_of(e_tile + int64_t(u * kThreads + threadIdx.x) * GROUP);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t e0 = e_tile + int64_t(u * kThreads + threadIdx.x) * GROUP;
+          uint32_t w[VEC];
+          decode_group<BF16, VEC, PRMT>(lut, q[u], a[u], w);
+          st_group<VEC>(d.out + e0, w);
+        }
+      } else {
+        for (int u = 0; u < U; ++u) {
+          const int64_t e0 = e_tile + int64_t(u * kThreads + threadIdx.x) * GROUP;
+          if (e0 >= d.n) break;
+          const float a = scale_of(e0);  // GROUP | blocksize: one block per group
+          if (d.vec_ok && e0 + GROUP <= d.n) {
+            uint32_t w[VEC];
+            decode_group<BF16, VEC, PRMT>(lut, ld_codes<VEC>(d.packed + (e0 >> 1)), a, w);
+            st_group<VEC>(d.out + e0, w);
+          } else {
+            slow_group<BF16, GROUP>(d, lut, e0, a);
+          }
         }
       }
+      if (SSCALE) __syncthreads();  // sscale is rewritten for the next tile
     }
+    if (!CLC) break;
+    mbar_wait(&clc_bar, phase);
+    phase ^= 1;
+    cta = clc_result(&clc_res);
+    __syncthreads();  // every thread has read clc_res before the next try_cancel overwrites it
+    if (cta < 0) break;
   }
 }
 
 // ---------------------------------------------------------------------------
 // Host side
 // ---------------------------------------------------------------------------
-static int occupancy(bool bf16) {
+using KernelFn = void (*)(BatchParams);
+
+template <bool BF16>
+static KernelFn kernel_for(int v) {
+  switch (v) {
+    case 0: return dequant_kernel<BF16, 8, 4, false, false, false, false>;
+    case 1: return dequant_kernel<BF16, 16, 2, false, false, false, false>;
+    case 2: return dequant_kernel<BF16, 16, 4, false, false, false, false>;
+    case 3: return dequant_kernel<BF16, 8, 4, true, false, false, false>;
+    case 4: return dequant_kernel<BF16, 16, 1, false, false, false, false>;
+    case 5: return dequant_kernel<BF16, 8, 8, false, false, false, false>;
+    case 6: return dequant_kernel<BF16, 8, 4, false, true, false, false>;
+    case 7: return dequant_kernel<BF16, 8, 4, false, true, true, false>;
+    case 8: return dequant_kernel<BF16, 8, 4, false, true, true, true>;
+    case 9: return dequant_kernel<BF16, 8, 4, false, false, false, true>;
+    default: return dequant_kernel<BF16, 8, 4, false, false, true, true>;
+  }
+}
+
+static std::atomic<int> g_variant{-1};
+
+static int current_variant() {
+  int v = g_variant.load(std::memory_order_relaxed);
+  if (v >= 0) return v;
+  v = kDefaultVariant;
+  if (const char* env = getenv("NF4_KERNEL_VARIANT")) {
+    for (int i = 0; i < kNumVariants; ++i)
+      if (strcmp(env, kVariants[i].name) == 0) v = i;
+    if (env[0] >= '0' && env[0] <= '9' && atoi(env) < kNumVariants) v = atoi(env);
+  }
+  g_variant.store(v, std::memory_order_relaxed);
+  return v;
+}
+
+static int64_t tile_elems(int v) { return int64_t(kThreads) * 2 * kVariants[v].vec * kVariants[v].unroll; }
+
+static int occupancy(int v, bool bf16) {
   static std::mutex mu;
-  static int cache[2] = {0, 0};
+  static int cache[kNumVariants][2] = {};
   std::lock_guard<std::mutex> g(mu);
-  int& c = cache[bf16 ? 1 : 0];
+  int& c = cache[v][bf16 ? 1 : 0];
   if (c == 0) {
-    int v = 0;
-    cudaError_t e = bf16 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, dequant_kernel<true>, kThreads, 0)
-                         : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, dequant_kernel<false>, kThreads, 0);
-    c = (e == cudaSuccess && v > 0) ? v : 4;
+    int occ = 0;
+    const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &occ, reinterpret_cast<const void*>(bf16 ? kernel_for<true>(v) : kernel_for<false>(v)), kThreads, 0);
+    c = (e == cudaSuccess && occ > 0) ? occ : 4;
   }
   return c;
 }
 
-static int grid_for(int64_t tiles, bool bf16) {
-  int64_t g = int64_t(sm_count()) * occupancy(bf16);
+static int grid_for(int v, int64_t tiles, bool bf16) {
+  int64_t g = kVariants[v].persist ? int64_t(sm_count()) * occupancy(v, bf16) : tiles;
   const int32_t cap = max_ctas();
   if (cap > 0 && g > cap) g = cap;
   if (g > tiles) g = tiles;
+  if (g > 0x7FFFFFFF) g = 0x7FFFFFFF;
   return int(g < 1 ? 1 : g);
 }
 
@@ -189,6 +395,8 @@ static nf4_status validate(const nf4_tensor& t, bool* has_work) {
 
 static nf4_status launch_batch(const nf4_tensor* ts, int count, bool bf16, cudaStream_t stream,
                                int32_t* launches) {
+  const int v = current_variant();
+  const int64_t tile = tile_elems(v);
   BatchParams P;
   P.count = 0;
   P.pad_ = 0;
@@ -206,18 +414,16 @@ static nf4_status launch_batch(const nf4_tensor* ts, int count, bool bf16, cudaS
     d.out = static_cast<uint16_t*>(t.out);
     d.n = t.n;
     d.bs_shift = log2i(t.blocksize);
-    d.vec_ok = aligned(t.packed, 8) && aligned(t.out, 32);
+    d.vec_ok = aligned(t.packed, kVariants[v].vec) && aligned(t.out, 32);
     d.pad_ = 0;
-    tiles += (t.n + kTile - 1) / kTile;
+    tiles += (t.n + tile - 1) / tile;
     d.tile_end = tiles;
   }
   if (P.count == 0) return NF4_OK;
   P.total_tiles = tiles;
-  const int grid = grid_for(tiles, bf16);
-  if (bf16)
-    dequant_kernel<true><<<grid, kThreads, 0, stream>>>(P);
-  else
-    dequant_kernel<false><<<grid, kThreads, 0, stream>>>(P);
+  const int grid = grid_for(v, tiles, bf16);
+  KernelFn fn = bf16 ? kernel_for<true>(v) : kernel_for<false>(v);
+  fn<<<grid, kThreads, 0, stream>>>(P);
   const cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) {
     cudaGetLastError();
@@ -294,5 +500,17 @@ extern "C" void nf4_codebook(float out16[16]) {
   }
 }
 
-extern "C" int32_t nf4_dequant_grid(int64_t tiles) { return grid_for(tiles < 1 ? 1 : tiles, false); }
-extern "C" int64_t nf4_dequant_tile_elems(void) { return kTile; }
+extern "C" int32_t nf4_dequant_grid(int64_t tiles) {
+  return grid_for(current_variant(), tiles < 1 ? 1 : tiles, false);
+}
+extern "C" int64_t nf4_dequant_tile_elems(void) { return tile_elems(current_variant()); }
+extern "C" int32_t nf4_kernel_variant_count(void) { return kNumVariants; }
+extern "C" const char* nf4_kernel_variant_name(int32_t v) {
+  return (v >= 0 && v < kNumVariants) ? kVariants[v].name : nullptr;
+}
+extern "C" int32_t nf4_set_kernel_variant(int32_t v) {
+  if (v < 0 || v >= kNumVariants) return current_variant();
+  g_variant.store(v, std::memory_order_relaxed);
+  return v;
+}
+extern "C" int32_t nf4_get_kernel_variant(void) { return current_variant(); }

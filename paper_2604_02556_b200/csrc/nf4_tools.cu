@@ -49,23 +49,30 @@ __global__ void synth_f32_kernel(uint64_t seed, uint64_t stream, int64_t begin, 
 }
 
 // ---------------------------------------------------------------------------
-// Speed-of-light stream with the dequant kernel's exact access pattern:
-// per thread and tile, 4 x 8-byte loads (warp-contiguous 256 B) and
-// 4 x 32-byte evict-first stores (warp-contiguous 1 KB); no table, no math.
+// Speed-of-light stream with the default dequant variant's access pattern
+// (v4u2): per thread and tile, 2 x 16-byte loads (warp-contiguous 512 B) and
+// 2 x 64 B thread-contiguous stores (2 x STG.256), one CTA per 8 KB-input tile;
+// no table, no math.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) sol_stream_kernel(const uint8_t* __restrict__ src, int64_t in_bytes,
                                                          uint8_t* __restrict__ dst) {
-  const int64_t tiles = in_bytes / 8192;  // 8 KB of input per tile (= 16384 elements)
+  const int64_t tiles = in_bytes / 8192;
   for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-    uint2 q[4];
+    uint4 q[2];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) q[u] = ld_codes_v2(src + t * 8192 + (u * 256 + threadIdx.x) * 8);
+    for (int u = 0; u < 2; ++u) {
+      const uint8_t* p = src + t * 8192 + (u * 256 + threadIdx.x) * 16;
+      asm("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+          : "=r"(q[u].x), "=r"(q[u].y), "=r"(q[u].z), "=r"(q[u].w) : "l"(p));
+    }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      uint32_t w[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) w[j] = (j < 4 ? q[u].x : q[u].y) * 0x00010001u;
-      st_out_v8(dst + (t * 8192 + (u * 256 + threadIdx.x) * 8) * 4, w);
+    for (int u = 0; u < 2; ++u) {
+      uint8_t* o = dst + (t * 8192 + (u * 256 + threadIdx.x) * 16) * 4;
+      const uint32_t x = q[u].x * 0x10001u, y = q[u].y * 0x10001u, z = q[u].z * 0x10001u, w = q[u].w * 0x10001u;
+      const uint32_t a[8] = {x, x, x, x, y, y, y, y};
+      const uint32_t b[8] = {z, z, z, z, w, w, w, w};
+      st_out_v8(o, a);
+      st_out_v8(o + 32, b);
     }
   }
 }
@@ -109,17 +116,10 @@ extern "C" nf4_status nf4_sol_stream(const void* src, int64_t in_bytes, void* ds
   if (in_bytes == 0) { set_launch_count(0); return NF4_OK; }
   if (!src || !dst) return NF4_ERR_NULL_POINTER;
   if (!aligned(src, 32) || !aligned(dst, 128)) return NF4_ERR_MISALIGNED;
-  static int occ = 0;
-  if (occ == 0) {
-    int v = 0;
-    occ = (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, sol_stream_kernel, 256, 0) == cudaSuccess && v > 0)
-              ? v : 4;
-  }
-  int64_t grid = int64_t(sm_count()) * occ;
+  int64_t grid = in_bytes / 8192;  // one CTA per tile (hardware-scheduled)
   const int32_t cap = max_ctas();
   if (cap > 0 && grid > cap) grid = cap;
-  const int64_t tiles = in_bytes / 8192;
-  if (grid > tiles) grid = tiles;
+  if (grid > 0x7FFFFFFF) grid = 0x7FFFFFFF;
   sol_stream_kernel<<<int(grid), 256, 0, (cudaStream_t)stream>>>(static_cast<const uint8_t*>(src), in_bytes,
                                                                  static_cast<uint8_t*>(dst));
   if (cudaPeekAtLastError() != cudaSuccess) { cudaGetLastError(); return NF4_ERR_CUDA; }

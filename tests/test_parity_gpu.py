@@ -108,6 +108,24 @@ def test_parity_special_values(nf4, orc):
         assert npref.same_bits(got, ref, dtype).all()
 
 
+@pytest.mark.parametrize("dq", [False, True])
+def test_all_kernel_variants_bit_exact(nf4, orc, dq):
+    """Every dequant variant (vector width, unroll, persistent or one CTA per
+    tile) gives the oracle's bytes, including tails and small tensors."""
+    names = nf4.nf4_kernel_variants()
+    default = nf4.nf4_get_kernel_variant()
+    try:
+        for v in range(len(names)):
+            assert nf4.nf4_set_kernel_variant(v) == v
+            for dtype in ("f16", "bf16"):
+                for n in (1, 33, 1025, 2 * TILE - 7, 5 * TILE, 9 * TILE + 4099):
+                    packed, kw = _inputs(n, 64, dq, 3 * n + v)
+                    got = host16(_gpu_deq(nf4, packed, kw, n, 64, dtype))
+                    assert np.array_equal(got, _oracle(orc, packed, kw, n, 64, dtype)), (names[v], dtype, n)
+    finally:
+        nf4.nf4_set_kernel_variant(default)
+
+
 def test_grid_size_invariance(nf4, orc):
     """Identical bytes for 1 CTA, one wave, and the automatic persistent grid."""
     import torch
@@ -358,8 +376,7 @@ def test_sol_stream(nf4):
     dst = torch.empty(src.numel() * 4, dtype=torch.uint8, device="cuda")
     nf4.nf4_sol_stream(src, src.numel(), dst)
     torch.cuda.synchronize()
-    s = src.cpu().numpy().view(np.uint32).reshape(-1, 2).astype(np.uint64)
-    d = dst.cpu().numpy().view(np.uint32).reshape(-1, 8)
-    x = ((s[:, 0] * 0x00010001) & 0xFFFFFFFF).astype(np.uint32)
-    y = ((s[:, 1] * 0x00010001) & 0xFFFFFFFF).astype(np.uint32)
-    assert np.array_equal(d, np.stack([x, x, x, x, y, y, y, y], 1))
+    s = src.cpu().numpy().view(np.uint32).astype(np.uint64)
+    d = dst.cpu().numpy().view(np.uint32).reshape(-1, 4)
+    x = ((s * 0x00010001) & 0xFFFFFFFF).astype(np.uint32)
+    assert np.array_equal(d, np.stack([x, x, x, x], 1))
