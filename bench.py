@@ -190,10 +190,7 @@ def run_reference(args, rank, world):
 def build_store(args, rank, world, device):
     from paper_2604_02556_b200 import weights
     c = wl.CONFIGS[args.config]
-    if args.scaling == "strong":
-        tensors = wl.config_tensors(args.config, world_size=world, rank=rank, layers=args.layers)
-    else:
-        tensors = wl.config_tensors(args.config, layers=args.layers)
+    tensors = rank_tensors(args.config, args.scaling, world, rank, args.layers)
     seed0 = 1000 * int(args.config[-1]) + 100000 * rank
     maker = weights.from_gaussian if args.inputs == "gaussian" else weights.from_hash
     return maker(tensors, c.blocksize, c.dq, c.out_dtype, seed0=seed0, device=device), tensors
@@ -279,6 +276,27 @@ def run_e2e(nf4, torch, ws, args, max_host_bytes):
                       f"pinned host buffers, {chunk}-element chunks"}
 
 
+def reduce_over_ranks(ms: float, alg_bytes: float, elems: float, device, world: int):
+    """Max of the per-rank timed-region milliseconds and sum of the per-rank work
+    (algorithmic bytes, elements) -- the only cross-rank traffic of the path."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    u = torch.tensor([alg_bytes, elems], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(u, op=dist.ReduceOp.SUM)
+    return float(t.item()), float(u[0].item()), float(u[1].item())
+
+
+def rank_tensors(cfg: str, scaling: str, world: int, rank: int, layers=None):
+    """Tensors rank `rank` dequantizes: its row shard of every weight (strong)
+    or a full linear-weight set of its own (weak)."""
+    if scaling == "strong":
+        return wl.config_tensors(cfg, world_size=world, rank=rank, layers=layers)
+    return wl.config_tensors(cfg, layers=layers)
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -355,13 +373,8 @@ def run_ours(args, rank, world, local_rank):
         dist.barrier()
     clocks = sampler.stop()
     ms = start.elapsed_time(end)
-    t_max = torch.tensor([ms], dtype=torch.float64, device=device)
-    units = torch.tensor([float(ws.algorithmic_bytes()), float(ws.n_total)], dtype=torch.float64, device=device)
-    if world > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-        dist.all_reduce(units, op=dist.ReduceOp.SUM)
-    ms_max = float(t_max.item())
-    tot_bytes, tot_elems = float(units[0].item()), float(units[1].item())
+    ms_max, tot_bytes, tot_elems = reduce_over_ranks(ms, float(ws.algorithmic_bytes()), float(ws.n_total),
+                                                     device, world)
     value = tot_bytes * args.steps / (ms_max * 1e-3) / 1e9
     gelem = tot_elems * args.steps / (ms_max * 1e-3) / 1e9
 

@@ -48,6 +48,8 @@ constexpr int kThreads = 256;  // 8 warps per CTA
 //           launched CTA (clusterlaunchcontrol.try_cancel) and takes its tile,
 //           so the prologue (LUT staging, descriptor search) is paid once per
 //           CTA while tiles are still handed out in launch order
+//   (d)     double-buffered scale cache and CLC response slots: one CTA barrier
+//           per tile instead of three
 struct Variant {
   const char* name;
   int vec, unroll;
@@ -65,6 +67,7 @@ static const Variant kVariants[] = {
     {"v2u4sxc", 8, 4, false, true, true, true},      // 8
     {"v2u4c", 8, 4, false, false, false, true},      // 9
     {"v2u4xc", 8, 4, false, false, true, true},      // 10
+    {"v2u4sxcd", 8, 4, false, true, true, true},     // 11: + double-buffered scale cache / CLC slots
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 constexpr int kDefaultVariant = 8;   // v2u4sxc: best measured on B200 (profiles/r01_variants.md)
@@ -215,30 +218,37 @@ __device__ __forceinline__ int64_t clc_result(const uint4* result) {
   return ok ? int64_t(x) : -1;
 }
 
-template <bool BF16, int VEC, int U, bool PERSIST, bool SSCALE, bool PRMT, bool CLC>
+template <bool BF16, int VEC, int U, bool PERSIST, bool SSCALE, bool PRMT, bool CLC, bool DB = false>
 __global__ void __launch_bounds__(kThreads) dequant_kernel(const __grid_constant__ BatchParams P) {
   constexpr int GROUP = 2 * VEC;                      // elements per thread-group
   constexpr int64_t TILE = int64_t(kThreads) * GROUP * U;
+  constexpr int NBUF = DB ? 2 : 1;                    // scale cache / CLC response slots
   static_assert(!SSCALE || TILE / 64 <= kMaxTileBlocks, "tile too large for the scale cache");
+  static_assert(!DB || (SSCALE && CLC), "double buffering needs the per-tile barrier of sscale");
   // A1: stage the 16-entry table in shared memory (16 banks, conflict-free).
   __shared__ float lut[16];
-  __shared__ float sscale[SSCALE ? kMaxTileBlocks : 1];
-  __shared__ __align__(16) uint4 clc_res;
-  __shared__ __align__(8) uint64_t clc_bar;
+  __shared__ float sscale[NBUF][SSCALE ? kMaxTileBlocks : 1];
+  __shared__ __align__(16) uint4 clc_res[NBUF];
+  __shared__ __align__(8) uint64_t clc_bar[NBUF];
   if (threadIdx.x < 16) lut[threadIdx.x] = __uint_as_float(c_nf4_bits[threadIdx.x]);
   if (CLC && threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
-        static_cast<uint32_t>(__cvta_generic_to_shared(&clc_bar))) : "memory");
+    for (int i = 0; i < NBUF; ++i)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+          static_cast<uint32_t>(__cvta_generic_to_shared(&clc_bar[i]))) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
   int cur = 0;
-  uint32_t phase = 0;
+  uint32_t it = 0;           // tiles processed by this CTA (scale-cache slot)
+  uint32_t ci = 0;           // CTA ids processed by this CTA (CLC slot / phase)
   int64_t cta = blockIdx.x;  // CTA id whose tiles we process (own, then stolen ones)
   while (true) {
-    if (CLC && threadIdx.x == 0) clc_try_cancel(&clc_res, &clc_bar);
-    for (int64_t tile = cta; tile < P.total_tiles; tile += gridDim.x) {
+    const int cs = DB ? int(ci & 1) : 0;
+    // Safe to overwrite clc_res[cs]: with DB every thread read it two CTA ids ago
+    // and has since passed the per-tile barrier; without DB, the barrier below.
+    if (CLC && threadIdx.x == 0) clc_try_cancel(&clc_res[cs], &clc_bar[cs]);
+    for (int64_t tile = cta; tile < P.total_tiles; tile += gridDim.x, ++it) {
       if (PERSIST || CLC) {  // tiles arrive (mostly) in increasing order: walk a cursor
         while (tile >= P.t[cur].tile_end) ++cur;
         while (cur > 0 && tile < P.t[cur - 1].tile_end) --cur;
@@ -254,17 +264,20 @@ __global__ void __launch_bounds__(kThreads) dequant_kernel(const __grid_constant
       const int64_t first = cur == 0 ? 0 : P.t[cur - 1].tile_end;
       const int64_t e_tile = (tile - first) * TILE;
       const bool full = d.vec_ok && e_tile + TILE <= d.n;
+      float* ss = sscale[DB ? (it & 1) : 0];
 
       if (SSCALE) {
-        // A4 once per quantization block of this tile (one thread per block)
+        // A4 once per quantization block of this tile (one thread per block).
+        // With DB this slot was last read two tiles ago, before the previous
+        // tile's barrier, so one barrier per tile suffices.
         const int64_t b0 = e_tile >> d.bs_shift;
         const int64_t nb = (d.n + (int64_t(1) << d.bs_shift) - 1) >> d.bs_shift;
         const int nblk = int(((TILE - 1) >> d.bs_shift) + 1);
-        if (int(threadIdx.x) < nblk && b0 + threadIdx.x < nb) sscale[threadIdx.x] = block_scale(d, b0 + threadIdx.x);
+        if (int(threadIdx.x) < nblk && b0 + threadIdx.x < nb) ss[threadIdx.x] = block_scale(d, b0 + threadIdx.x);
         __syncthreads();
       }
       auto scale_of = [&](int64_t e0) -> float {
-        return SSCALE ? sscale[(e0 - e_tile) >> d.bs_shift] : block_scale(d, e0 >> d.bs_shift);
+        return SSCALE ? ss[(e0 - e_tile) >> d.bs_shift] : block_scale(d, e0 >> d.bs_shift);
       };
 
       if (full) {
@@ -298,13 +311,13 @@ __global__ void __launch_bounds__(kThreads) dequant_kernel(const __grid_constant
           }
         }
       }
-      if (SSCALE) __syncthreads();  // sscale is rewritten for the next tile
+      if (SSCALE && !DB) __syncthreads();  // sscale is rewritten for the next tile
     }
     if (!CLC) break;
-    mbar_wait(&clc_bar, phase);
-    phase ^= 1;
-    cta = clc_result(&clc_res);
-    __syncthreads();  // every thread has read clc_res before the next try_cancel overwrites it
+    mbar_wait(&clc_bar[cs], DB ? ((ci >> 1) & 1) : (ci & 1));
+    cta = clc_result(&clc_res[cs]);
+    ++ci;
+    if (!DB) __syncthreads();  // every thread has read clc_res before the next try_cancel
     if (cta < 0) break;
   }
 }
@@ -327,7 +340,8 @@ static KernelFn kernel_for(int v) {
     case 7: return dequant_kernel<BF16, 8, 4, false, true, true, false>;
     case 8: return dequant_kernel<BF16, 8, 4, false, true, true, true>;
     case 9: return dequant_kernel<BF16, 8, 4, false, false, false, true>;
-    default: return dequant_kernel<BF16, 8, 4, false, false, true, true>;
+    case 10: return dequant_kernel<BF16, 8, 4, false, false, true, true>;
+    default: return dequant_kernel<BF16, 8, 4, false, true, true, true, true>;
   }
 }
 
