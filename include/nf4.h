@@ -48,7 +48,7 @@ typedef enum {
 typedef enum {
   NF4_F16 = 0,   /* IEEE binary16, round-to-nearest-even from the fp32 product (R5) */
   NF4_BF16 = 1,  /* bfloat16, round-to-nearest-even (R6)                                   */
-  NF4_F32 = 2    /* fp32: only as the input dtype of nf4_quantize                          */
+  NF4_F32 = 2    /* fp32: input dtype of nf4_quantize; output dtype of nf4_dequantize_ex   */
 } nf4_dtype;
 
 /* Double-quantized ("nested", QLoRA) absmax state; R7.  The per-block scale is
@@ -158,8 +158,28 @@ nf4_status nf4_quantize(const void* in, nf4_dtype in_dtype, int64_t n, int32_t b
 nf4_status nf4_double_quantize(const float* absmax, int64_t nb, float offset, const float* code2,
                                int32_t blocksize2, uint8_t* qabsmax, float* absmax2, void* stream);
 
+/*
+ * nf4_dequantize_ex / nf4_dequantize_batched_ex -- the same path with another
+ * 16-entry codebook and/or fp32 output.
+ *   codebook16 [host] 16 fp32 levels indexed by the 4-bit code, or NULL for NF4
+ *              (e.g. nf4_codebook_fp4 for the BitsAndBytes FP4 format).  Read
+ *              during the call only; copied into the kernel parameters.
+ *   out_dtype  NF4_F16, NF4_BF16 or NF4_F32 (out[k] = the fp32 product itself;
+ *              `out` then holds n fp32 values, 4-byte aligned).
+ * Everything else as nf4_dequantize / nf4_dequantize_batched.
+ */
+nf4_status nf4_dequantize_ex(const uint8_t* packed, const float* absmax, const nf4_dq_state* dq,
+                             int64_t n, int32_t blocksize, const float* codebook16, nf4_dtype out_dtype,
+                             void* out, void* stream);
+nf4_status nf4_dequantize_batched_ex(const nf4_tensor* tensors, int32_t count, const float* codebook16,
+                                     nf4_dtype out_dtype, void* stream);
+
 /* Host copy of the 16-entry NF4 table (R1), fp32. */
 void nf4_codebook(float out16[16]);
+
+/* Host copy of the BitsAndBytes FP4 table ({0, 0.0625, 8, 12, 4, 6, 2, 3} and
+ * their negatives, divided by 12; [ext]) for nf4_dequantize_ex. */
+void nf4_codebook_fp4(float out16[16]);
 
 /* Static description of a status code; never NULL. */
 const char* nf4_status_string(nf4_status s);

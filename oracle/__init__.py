@@ -28,6 +28,7 @@ _lib = None
 
 OUT_F16 = 0
 OUT_BF16 = 1
+OUT_F32 = 2
 
 CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared"]
 
@@ -59,6 +60,8 @@ def _load():
             lib.oracle_f32_to_bf16_bulk.argtypes = [P, i64, P]
             lib.oracle_dequantize.argtypes = [P, P, P, P, P, f32, i32, i64, i32, i32, i64, i64, P]
             lib.oracle_dequantize.restype = ctypes.c_int
+            lib.oracle_dequantize_ex.argtypes = [P, P, P, P, P, f32, i32, i64, i32, P, i32, i64, i64, P]
+            lib.oracle_dequantize_ex.restype = ctypes.c_int
             lib.oracle_quantize.argtypes = [P, i64, i32, P, P]
             lib.oracle_quantize.restype = ctypes.c_int
             lib.oracle_double_quantize.argtypes = [P, i64, f32, P, i32, P, P]
@@ -108,8 +111,10 @@ def f32_to_bf16_bits(x_bits: np.ndarray) -> np.ndarray:
 
 def dequantize(packed, n, blocksize, out_dtype, absmax=None, qabsmax=None, code2=None,
                absmax2=None, offset=0.0, blocksize2=256, k_begin=0, k_end=None,
-               threads: int = 1) -> np.ndarray:
-    """Oracle dequantization; returns the raw 16-bit output words (uint16).
+               threads: int = 1, codebook=None) -> np.ndarray:
+    """Oracle dequantization; returns the raw output words (uint16 for fp16/bf16,
+    uint32 fp32 bits for OUT_F32).  ``codebook``: optional 16-entry fp32 table
+    (default NF4).
 
     Exactly one of ``absmax`` (fp32 mode) or ``qabsmax``+``code2``+``absmax2``
     (double-quant mode) must be given.  ``threads`` > 1 splits [k_begin, k_end)
@@ -122,16 +127,20 @@ def dequantize(packed, n, blocksize, out_dtype, absmax=None, qabsmax=None, code2
     qabsmax = _c(qabsmax, np.uint8)
     code2 = _c(code2, np.float32)
     absmax2 = _c(absmax2, np.float32)
+    cb = _c(codebook, np.float32)
+    if cb is not None and cb.size != 16:
+        raise ValueError("codebook must have 16 entries")
     if k_end is None:
         k_end = n
     m = k_end - k_begin
-    out = np.empty(max(m, 0), np.uint16)
+    wsz = 4 if out_dtype == OUT_F32 else 2
+    out = np.empty(max(m, 0), np.uint32 if wsz == 4 else np.uint16)
 
     def run(a, b):
-        rc = lib.oracle_dequantize(_ptr(packed), _ptr(absmax), _ptr(qabsmax), _ptr(code2),
-                                   _ptr(absmax2), float(offset), int(blocksize2), int(n),
-                                   int(blocksize), int(out_dtype), int(a), int(b),
-                                   out.ctypes.data + 2 * (a - k_begin))
+        rc = lib.oracle_dequantize_ex(_ptr(packed), _ptr(absmax), _ptr(qabsmax), _ptr(code2),
+                                      _ptr(absmax2), float(offset), int(blocksize2), int(n),
+                                      int(blocksize), _ptr(cb), int(out_dtype), int(a), int(b),
+                                      out.ctypes.data + wsz * (a - k_begin))
         if rc != 0:
             raise ValueError(f"oracle_dequantize rejected its arguments (rc={rc})")
 

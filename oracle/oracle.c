@@ -31,6 +31,7 @@
 
 #define OR_OUT_F16 0
 #define OR_OUT_BF16 1
+#define OR_OUT_F32 2
 
 /* ---------------------------------------------------------------------
  * NF4 codebook.  P:67: "16 ... levels following quantile values of a
@@ -151,31 +152,49 @@ static float decode_absmax(int64_t b, const float* absmax,
  *     idx  = (k even) ? byte >> 4 : byte & 0x0F      high nibble first, P:160-161 (R2)
  *     b    = k / blocksize                          scale index (R3)
  *     a    = decode_absmax(b)                       A4 (R7)
- *     p    = fl32(NF4[idx] * a)                     fp32 product, P:160, P:122 (R5)
+ *     p    = fl32(CB[idx] * a)                      fp32 product, P:160, P:122 (R5)
  *     out[k - k_begin] = RNE16(p)                   fp16 or bf16 (R6)
+ *                      = p                          fp32 output
+ * CB is the NF4 table unless `codebook16` supplies another 16-entry table
+ * (e.g. the BitsAndBytes FP4 table).  `out` holds uint16
+ * words for fp16/bf16 and uint32 words (fp32 bits) for fp32.
  * Exactly one of `absmax` (fp32 mode) and `qabsmax` (DQ mode) is non-NULL.
  * Returns OR_OK, or OR_ERR_ARG on an invalid argument (nothing written).
  * ------------------------------------------------------------------- */
-int oracle_dequantize(const uint8_t* packed, const float* absmax,
-                      const uint8_t* qabsmax, const float* code2,
-                      const float* absmax2, float offset, int32_t blocksize2,
-                      int64_t n, int32_t blocksize, int32_t out_dtype,
-                      int64_t k_begin, int64_t k_end, uint16_t* out) {
+int oracle_dequantize_ex(const uint8_t* packed, const float* absmax,
+                         const uint8_t* qabsmax, const float* code2,
+                         const float* absmax2, float offset, int32_t blocksize2,
+                         int64_t n, int32_t blocksize, const float* codebook16,
+                         int32_t out_dtype, int64_t k_begin, int64_t k_end, void* out) {
     if (n < 0 || blocksize <= 0 || k_begin < 0 || k_end > n || k_begin > k_end) return OR_ERR_ARG;
     if ((absmax == 0) == (qabsmax == 0)) return OR_ERR_ARG;
     if (qabsmax != 0 && (code2 == 0 || absmax2 == 0 || blocksize2 <= 0)) return OR_ERR_ARG;
-    if (out_dtype != OR_OUT_F16 && out_dtype != OR_OUT_BF16) return OR_ERR_ARG;
+    if (out_dtype != OR_OUT_F16 && out_dtype != OR_OUT_BF16 && out_dtype != OR_OUT_F32) return OR_ERR_ARG;
+    float cb[16];
+    for (int i = 0; i < 16; i++) cb[i] = codebook16 ? codebook16[i] : bits_to_f32(NF4_BITS[i]);
     for (int64_t k = k_begin; k < k_end; k++) {
         uint8_t byte = packed[k >> 1];
         uint32_t idx = (k % 2 == 0) ? (uint32_t)(byte >> 4) : (uint32_t)(byte & 0x0F);
         int64_t b = k / blocksize;
         float a = decode_absmax(b, absmax, qabsmax, code2, absmax2, offset, blocksize2);
-        float c = bits_to_f32(NF4_BITS[idx]);
-        float p = c * a;
+        float p = cb[idx] * a;
         uint32_t pb = f32_to_bits(p);
-        out[k - k_begin] = (out_dtype == OR_OUT_F16) ? oracle_f32_to_f16(pb) : oracle_f32_to_bf16(pb);
+        if (out_dtype == OR_OUT_F32)       ((uint32_t*)out)[k - k_begin] = pb;
+        else if (out_dtype == OR_OUT_F16)  ((uint16_t*)out)[k - k_begin] = oracle_f32_to_f16(pb);
+        else                               ((uint16_t*)out)[k - k_begin] = oracle_f32_to_bf16(pb);
     }
     return OR_OK;
+}
+
+/* The paper's configuration: NF4 table, fp16/bf16 output. */
+int oracle_dequantize(const uint8_t* packed, const float* absmax,
+                      const uint8_t* qabsmax, const float* code2,
+                      const float* absmax2, float offset, int32_t blocksize2,
+                      int64_t n, int32_t blocksize, int32_t out_dtype,
+                      int64_t k_begin, int64_t k_end, uint16_t* out) {
+    if (out_dtype != OR_OUT_F16 && out_dtype != OR_OUT_BF16) return OR_ERR_ARG;
+    return oracle_dequantize_ex(packed, absmax, qabsmax, code2, absmax2, offset, blocksize2,
+                                n, blocksize, 0, out_dtype, k_begin, k_end, out);
 }
 
 /* ---------------------------------------------------------------------

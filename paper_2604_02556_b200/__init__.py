@@ -25,6 +25,7 @@ __all__ = [
     "nf4_quantize", "nf4_double_quantize", "nf4_codebook", "nf4_last_launch_count",
     "nf4_synth_fill", "nf4_sol_stream", "nf4_set_max_ctas", "nf4_dequant_grid", "nf4_dequant_tile_elems",
     "nf4_kernel_variants", "nf4_set_kernel_variant", "nf4_get_kernel_variant",
+    "nf4_dequantize_ex", "nf4_dequantize_batched_ex", "nf4_codebook_fp4",
 ]
 
 
@@ -111,6 +112,48 @@ def nf4_dequantize(packed, absmax=None, dq: Optional[DQ] = None, *, n: int, bloc
                                int(n), int(blocksize), code, _ptr(out), _stream(stream))
     _lib.check(st, "nf4_dequantize")
     return out
+
+
+def _codebook_arg(codebook):
+    if codebook is None:
+        return None
+    if isinstance(codebook, str):
+        codebook = nf4_codebook_fp4() if codebook == "fp4" else nf4_codebook() if codebook == "nf4" else None
+        if codebook is None:
+            raise ValueError("codebook must be 'nf4', 'fp4' or 16 floats")
+    vals = [float(v) for v in (codebook.tolist() if hasattr(codebook, "tolist") else codebook)]
+    if len(vals) != 16:
+        raise ValueError("codebook must have 16 entries")
+    return (ctypes.c_float * 16)(*vals)
+
+
+def nf4_dequantize_ex(packed, absmax=None, dq: Optional[DQ] = None, *, n: int, blocksize: int = 64,
+                      codebook=None, out_dtype="f16", out=None, stream=None):
+    """nf4_dequantize with another 16-entry codebook ('fp4', 'nf4' or 16 floats)
+    and/or fp32 output."""
+    import torch
+    code = _dtype_code(out_dtype)
+    if out is None:
+        tdt = {_lib.NF4_F16: torch.float16, _lib.NF4_BF16: torch.bfloat16, _lib.NF4_F32: torch.float32}[code]
+        out = torch.empty(n, dtype=tdt, device=packed.device)
+    dqc = dq.c() if dq is not None else None
+    st = load().nf4_dequantize_ex(_ptr(packed), _ptr(absmax), ctypes.byref(dqc) if dqc is not None else None,
+                                  int(n), int(blocksize), _codebook_arg(codebook), code, _ptr(out), _stream(stream))
+    _lib.check(st, "nf4_dequantize_ex")
+    return out
+
+
+def nf4_dequantize_batched_ex(tensors: Sequence[NF4Tensor], codebook=None, out_dtype="f16", stream=None) -> None:
+    arr = (_lib.TensorDesc * max(len(tensors), 1))(*[t.c() for t in tensors])
+    st = load().nf4_dequantize_batched_ex(arr, len(tensors), _codebook_arg(codebook), _dtype_code(out_dtype),
+                                          _stream(stream))
+    _lib.check(st, "nf4_dequantize_batched_ex")
+
+
+def nf4_codebook_fp4():
+    buf = (ctypes.c_float * 16)()
+    load().nf4_codebook_fp4(buf)
+    return list(buf)
 
 
 def nf4_dequantize_batched(tensors: Sequence[NF4Tensor], out_dtype="f16", stream=None) -> None:

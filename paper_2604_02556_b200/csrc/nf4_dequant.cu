@@ -1,4 +1,4 @@
-// nf4_dequant.cu -- B200 (sm_100a) blockwise NF4 -> FP16/BF16 dequantization.
+// nf4_dequant.cu -- B200 (sm_100a) blockwise NF4 -> FP16/BF16 (and FP32) dequantization.
 //
 // The hot path of arxiv 2604.02556 (Alg. 1): unpack two 4-bit codes
 // per byte (high nibble first), look each up in the 16-entry NF4
@@ -79,7 +79,7 @@ struct TensorDesc {
   const uint8_t* qabsmax; // DQ mode otherwise
   const float* code2;
   const float* absmax2;
-  uint16_t* out;
+  void* out;              // uint16 words (fp16/bf16) or fp32
   int64_t n;
   int64_t tile_end;       // exclusive prefix of tiles over the batch
   float offset;
@@ -92,6 +92,7 @@ struct BatchParams {
   int64_t total_tiles;
   int32_t count;
   int32_t pad_;
+  float lut[16];          // the 16-entry codebook (NF4 unless nf4_dequantize_ex supplies one)
   TensorDesc t[NF4_MAX_BATCH];
 };
 
@@ -130,9 +131,27 @@ __device__ __forceinline__ float lut_at(const float* lut, uint32_t byte_off) {
 // 2*VEC elements from VEC code bytes: element 2j <- high nibble of byte j
 // (P:160-161), product fl32(NF4[idx] * a), RNE to 16 bits;
 // word j holds elements (2j, 2j+1) with 2j in the low half.
-template <bool BF16, int VEC, bool PRMT>
+// Output words per thread-group: VEC 32-bit words (two 16-bit results each),
+// or 2*VEC words for fp32 output.
+template <int OUT, int VEC>
+struct OutWords {
+  static constexpr int value = OUT == 2 ? 2 * VEC : VEC;
+};
+
+// Store the products of elements (2j, 2j+1) as output word(s) j.
+template <int OUT, int VEC>
+__device__ __forceinline__ void put_pair(uint32_t (&w)[OutWords<OUT, VEC>::value], int j, float ph, float pl) {
+  if constexpr (OUT == 2) {
+    w[2 * j] = __float_as_uint(ph);
+    w[2 * j + 1] = __float_as_uint(pl);
+  } else {
+    w[j] = pack2_rn<OUT == 1>(ph, pl);
+  }
+}
+
+template <int OUT, int VEC, bool PRMT>
 __device__ __forceinline__ void decode_group(const float* lut, const CodeVec<VEC>& q, float a,
-                                             uint32_t (&w)[VEC]) {
+                                             uint32_t (&w)[OutWords<OUT, VEC>::value]) {
   if constexpr (PRMT) {
 #pragma unroll
     for (int i = 0; i < VEC / 4; ++i) {
@@ -145,7 +164,7 @@ __device__ __forceinline__ void decode_group(const float* lut, const CodeVec<VEC
         const uint32_t ol = k == 0 ? (lo4 & 0xFFu) : k == 3 ? (lo4 >> 24) : __byte_perm(lo4, 0u, 0x4440u + k);
         const float ph = __fmul_rn(lut_at(lut, oh), a);  // element 2j
         const float pl = __fmul_rn(lut_at(lut, ol), a);  // element 2j+1
-        w[4 * i + k] = pack2_rn<BF16>(ph, pl);
+        put_pair<OUT, VEC>(w, 4 * i + k, ph, pl);
       }
     }
   } else {
@@ -154,28 +173,37 @@ __device__ __forceinline__ void decode_group(const float* lut, const CodeVec<VEC
       const uint32_t byte = (q.w[j >> 2] >> (8 * (j & 3))) & 0xFFu;
       const float ph = __fmul_rn(lut[byte >> 4], a);     // element 2j
       const float pl = __fmul_rn(lut[byte & 0x0Fu], a);  // element 2j+1
-      w[j] = pack2_rn<BF16>(ph, pl);
+      put_pair<OUT, VEC>(w, j, ph, pl);
     }
   }
 }
 
-template <int VEC>
-__device__ __forceinline__ void st_group(uint16_t* out, const uint32_t (&w)[VEC]) {
+template <int NW>
+__device__ __forceinline__ void st_group(void* out, const uint32_t (&w)[NW]) {
 #pragma unroll
-  for (int h = 0; h < VEC / 8; ++h) {
+  for (int h = 0; h < NW / 8; ++h) {
     const uint32_t(&ww)[8] = *reinterpret_cast<const uint32_t(*)[8]>(&w[8 * h]);
-    st_out_v8(out + 16 * h, ww);
+    st_out_v8(static_cast<uint8_t*>(out) + 32 * h, ww);
   }
 }
 
+template <int OUT>
+__device__ __forceinline__ void* out_at(const void* out, int64_t k) {
+  return const_cast<uint8_t*>(static_cast<const uint8_t*>(out)) + (OUT == 2 ? 4 : 2) * k;
+}
+
 // Element-wise path for tails and unaligned tensors.
-template <bool BF16, int GROUP>
+template <int OUT, int GROUP>
 __device__ __forceinline__ void slow_group(const TensorDesc& d, const float* lut, int64_t e0, float a) {
   const int64_t e1 = e0 + GROUP < d.n ? e0 + GROUP : d.n;
   for (int64_t k = e0; k < e1; ++k) {
     const uint32_t byte = d.packed[k >> 1];
     const uint32_t idx = (k & 1) ? (byte & 0x0Fu) : (byte >> 4);
-    d.out[k] = cvt1_rn<BF16>(__fmul_rn(lut[idx], a));
+    const float p = __fmul_rn(lut[idx], a);
+    if constexpr (OUT == 2)
+      static_cast<float*>(d.out)[k] = p;
+    else
+      static_cast<uint16_t*>(d.out)[k] = cvt1_rn<OUT == 1>(p);
   }
 }
 
@@ -218,7 +246,7 @@ __device__ __forceinline__ int64_t clc_result(const uint4* result) {
   return ok ? int64_t(x) : -1;
 }
 
-template <bool BF16, int VEC, int U, bool PERSIST, bool SSCALE, bool PRMT, bool CLC, bool DB = false>
+template <int OUT, int VEC, int U, bool PERSIST, bool SSCALE, bool PRMT, bool CLC, bool DB = false>
 __global__ void __launch_bounds__(kThreads) dequant_kernel(const __grid_constant__ BatchParams P) {
   constexpr int GROUP = 2 * VEC;                      // elements per thread-group
   constexpr int64_t TILE = int64_t(kThreads) * GROUP * U;
@@ -230,7 +258,7 @@ __global__ void __launch_bounds__(kThreads) dequant_kernel(const __grid_constant
   __shared__ float sscale[NBUF][SSCALE ? kMaxTileBlocks : 1];
   __shared__ __align__(16) uint4 clc_res[NBUF];
   __shared__ __align__(8) uint64_t clc_bar[NBUF];
-  if (threadIdx.x < 16) lut[threadIdx.x] = __uint_as_float(c_nf4_bits[threadIdx.x]);
+  if (threadIdx.x < 16) lut[threadIdx.x] = P.lut[threadIdx.x];  // kernel-parameter (constant) bank -> smem
   if (CLC && threadIdx.x == 0) {
     for (int i = 0; i < NBUF; ++i)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
@@ -293,9 +321,9 @@ __global__ void __launch_bounds__(kThreads) dequant_kernel(const __grid_constant
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int64_t e0 = e_tile + int64_t(u * kThreads + threadIdx.x) * GROUP;
-          uint32_t w[VEC];
-          decode_group<BF16, VEC, PRMT>(lut, q[u], a[u], w);
-          st_group<VEC>(d.out + e0, w);
+          uint32_t w[OutWords<OUT, VEC>::value];
+          decode_group<OUT, VEC, PRMT>(lut, q[u], a[u], w);
+          st_group(out_at<OUT>(d.out, e0), w);
         }
       } else {
         for (int u = 0; u < U; ++u) {
@@ -303,11 +331,11 @@ __global__ void __launch_bounds__(kThreads) dequant_kernel(const __grid_constant
           if (e0 >= d.n) break;
           const float a = scale_of(e0);  // GROUP | blocksize: one block per group
           if (d.vec_ok && e0 + GROUP <= d.n) {
-            uint32_t w[VEC];
-            decode_group<BF16, VEC, PRMT>(lut, ld_codes<VEC>(d.packed + (e0 >> 1)), a, w);
-            st_group<VEC>(d.out + e0, w);
+            uint32_t w[OutWords<OUT, VEC>::value];
+            decode_group<OUT, VEC, PRMT>(lut, ld_codes<VEC>(d.packed + (e0 >> 1)), a, w);
+            st_group(out_at<OUT>(d.out, e0), w);
           } else {
-            slow_group<BF16, GROUP>(d, lut, e0, a);
+            slow_group<OUT, GROUP>(d, lut, e0, a);
           }
         }
       }
@@ -327,21 +355,24 @@ __global__ void __launch_bounds__(kThreads) dequant_kernel(const __grid_constant
 // ---------------------------------------------------------------------------
 using KernelFn = void (*)(BatchParams);
 
-template <bool BF16>
+template <int OUT>
 static KernelFn kernel_for(int v) {
+  if constexpr (OUT == 2) {  // fp32 output (F4): only the default variant is instantiated
+    return dequant_kernel<2, 8, 4, false, true, true, true>;
+  }
   switch (v) {
-    case 0: return dequant_kernel<BF16, 8, 4, false, false, false, false>;
-    case 1: return dequant_kernel<BF16, 16, 2, false, false, false, false>;
-    case 2: return dequant_kernel<BF16, 16, 4, false, false, false, false>;
-    case 3: return dequant_kernel<BF16, 8, 4, true, false, false, false>;
-    case 4: return dequant_kernel<BF16, 16, 1, false, false, false, false>;
-    case 5: return dequant_kernel<BF16, 8, 8, false, false, false, false>;
-    case 6: return dequant_kernel<BF16, 8, 4, false, true, false, false>;
-    case 7: return dequant_kernel<BF16, 8, 4, false, true, true, false>;
-    case 8: return dequant_kernel<BF16, 8, 4, false, true, true, true>;
-    case 9: return dequant_kernel<BF16, 8, 4, false, false, false, true>;
-    case 10: return dequant_kernel<BF16, 8, 4, false, false, true, true>;
-    default: return dequant_kernel<BF16, 8, 4, false, true, true, true, true>;
+    case 0: return dequant_kernel<OUT, 8, 4, false, false, false, false>;
+    case 1: return dequant_kernel<OUT, 16, 2, false, false, false, false>;
+    case 2: return dequant_kernel<OUT, 16, 4, false, false, false, false>;
+    case 3: return dequant_kernel<OUT, 8, 4, true, false, false, false>;
+    case 4: return dequant_kernel<OUT, 16, 1, false, false, false, false>;
+    case 5: return dequant_kernel<OUT, 8, 8, false, false, false, false>;
+    case 6: return dequant_kernel<OUT, 8, 4, false, true, false, false>;
+    case 7: return dequant_kernel<OUT, 8, 4, false, true, true, false>;
+    case 8: return dequant_kernel<OUT, 8, 4, false, true, true, true>;
+    case 9: return dequant_kernel<OUT, 8, 4, false, false, false, true>;
+    case 10: return dequant_kernel<OUT, 8, 4, false, false, true, true>;
+    default: return dequant_kernel<OUT, 8, 4, false, true, true, true, true>;
   }
 }
 
@@ -362,22 +393,26 @@ static int current_variant() {
 
 static int64_t tile_elems(int v) { return int64_t(kThreads) * 2 * kVariants[v].vec * kVariants[v].unroll; }
 
-static int occupancy(int v, bool bf16) {
+static KernelFn kernel_of(int out, int v) {
+  return out == 0 ? kernel_for<0>(v) : out == 1 ? kernel_for<1>(v) : kernel_for<2>(v);
+}
+
+static int occupancy(int v, int out) {
   static std::mutex mu;
-  static int cache[kNumVariants][2] = {};
+  static int cache[kNumVariants][3] = {};
   std::lock_guard<std::mutex> g(mu);
-  int& c = cache[v][bf16 ? 1 : 0];
+  int& c = cache[v][out];
   if (c == 0) {
     int occ = 0;
     const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &occ, reinterpret_cast<const void*>(bf16 ? kernel_for<true>(v) : kernel_for<false>(v)), kThreads, 0);
+        &occ, reinterpret_cast<const void*>(kernel_of(out, v)), kThreads, 0);
     c = (e == cudaSuccess && occ > 0) ? occ : 4;
   }
   return c;
 }
 
-static int grid_for(int v, int64_t tiles, bool bf16) {
-  int64_t g = kVariants[v].persist ? int64_t(sm_count()) * occupancy(v, bf16) : tiles;
+static int grid_for(int v, int64_t tiles, int out) {
+  int64_t g = kVariants[v].persist ? int64_t(sm_count()) * occupancy(v, out) : tiles;
   const int32_t cap = max_ctas();
   if (cap > 0 && g > cap) g = cap;
   if (g > tiles) g = tiles;
@@ -385,8 +420,7 @@ static int grid_for(int v, int64_t tiles, bool bf16) {
   return int(g < 1 ? 1 : g);
 }
 
-static nf4_status validate(const nf4_tensor& t, bool* has_work) {
-  *has_work = false;
+static nf4_status validate(const nf4_tensor& t, int out) {
   if (t.n < 0) return NF4_ERR_BAD_SIZE;
   if (t.reserved != 0) return NF4_ERR_BAD_STATE;
   if (!is_pow2(t.blocksize) || t.blocksize < 64 || t.blocksize > 4096) return NF4_ERR_BAD_BLOCKSIZE;
@@ -400,20 +434,20 @@ static nf4_status validate(const nf4_tensor& t, bool* has_work) {
   if (t.n == 0) return NF4_OK;
   if (t.packed == nullptr || t.out == nullptr) return NF4_ERR_NULL_POINTER;
   if (dq && (t.dq.code2 == nullptr || t.dq.absmax2 == nullptr)) return NF4_ERR_NULL_POINTER;
-  if (!aligned(t.out, 2)) return NF4_ERR_MISALIGNED;
+  if (!aligned(t.out, out == 2 ? 4 : 2)) return NF4_ERR_MISALIGNED;
   if (!dq && !aligned(t.absmax, 4)) return NF4_ERR_MISALIGNED;
   if (dq && (!aligned(t.dq.code2, 4) || !aligned(t.dq.absmax2, 4))) return NF4_ERR_MISALIGNED;
-  *has_work = true;
   return NF4_OK;
 }
 
-static nf4_status launch_batch(const nf4_tensor* ts, int count, bool bf16, cudaStream_t stream,
+static nf4_status launch_batch(const nf4_tensor* ts, int count, int out, const float* lut, cudaStream_t stream,
                                int32_t* launches) {
-  const int v = current_variant();
+  const int v = out == 2 ? kDefaultVariant : current_variant();
   const int64_t tile = tile_elems(v);
   BatchParams P;
   P.count = 0;
   P.pad_ = 0;
+  for (int i = 0; i < 16; ++i) P.lut[i] = lut[i];
   int64_t tiles = 0;
   for (int i = 0; i < count; ++i) {
     const nf4_tensor& t = ts[i];
@@ -425,7 +459,7 @@ static nf4_status launch_batch(const nf4_tensor* ts, int count, bool bf16, cudaS
     d.code2 = t.absmax ? nullptr : t.dq.code2;
     d.absmax2 = t.absmax ? nullptr : t.dq.absmax2;
     d.offset = t.absmax ? 0.0f : t.dq.offset;
-    d.out = static_cast<uint16_t*>(t.out);
+    d.out = t.out;
     d.n = t.n;
     d.bs_shift = log2i(t.blocksize);
     d.vec_ok = aligned(t.packed, kVariants[v].vec) && aligned(t.out, 32);
@@ -435,8 +469,8 @@ static nf4_status launch_batch(const nf4_tensor* ts, int count, bool bf16, cudaS
   }
   if (P.count == 0) return NF4_OK;
   P.total_tiles = tiles;
-  const int grid = grid_for(v, tiles, bf16);
-  KernelFn fn = bf16 ? kernel_for<true>(v) : kernel_for<false>(v);
+  const int grid = grid_for(v, tiles, out);
+  KernelFn fn = kernel_of(out, v);
   fn<<<grid, kThreads, 0, stream>>>(P);
   const cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) {
@@ -447,19 +481,29 @@ static nf4_status launch_batch(const nf4_tensor* ts, int count, bool bf16, cudaS
   return NF4_OK;
 }
 
+static void nf4_table(float lut[16]) {
+  for (int i = 0; i < 16; ++i) memcpy(&lut[i], &h_nf4_bits[i], 4);
+}
+
 }  // namespace nf4
 
 using namespace nf4;
 
-extern "C" nf4_status nf4_dequantize_batched(const nf4_tensor* tensors, int32_t count, nf4_dtype out_dtype,
-                                             void* stream) {
+extern "C" nf4_status nf4_dequantize_batched_ex(const nf4_tensor* tensors, int32_t count, const float* codebook16,
+                                                nf4_dtype out_dtype, void* stream) {
   if (count < 0) return NF4_ERR_BAD_SIZE;
   if (count > 0 && tensors == nullptr) return NF4_ERR_NULL_POINTER;
-  if (out_dtype != NF4_F16 && out_dtype != NF4_BF16) return NF4_ERR_BAD_DTYPE;
+  if (out_dtype != NF4_F16 && out_dtype != NF4_BF16 && out_dtype != NF4_F32) return NF4_ERR_BAD_DTYPE;
+  const int out = int(out_dtype);
   for (int i = 0; i < count; ++i) {
-    bool w;
-    const nf4_status s = validate(tensors[i], &w);
+    const nf4_status s = validate(tensors[i], out);
     if (s != NF4_OK) return s;
+  }
+  float lut[16];
+  if (codebook16) {
+    for (int i = 0; i < 16; ++i) lut[i] = codebook16[i];
+  } else {
+    nf4_table(lut);
   }
   int32_t launches = 0;
   // Group tensors with work into launches of at most NF4_MAX_BATCH.
@@ -469,22 +513,28 @@ extern "C" nf4_status nf4_dequantize_batched(const nf4_tensor* tensors, int32_t 
     if (tensors[i].n == 0) continue;
     buf[nbuf++] = tensors[i];
     if (nbuf == NF4_MAX_BATCH) {
-      const nf4_status s = launch_batch(buf, nbuf, out_dtype == NF4_BF16, (cudaStream_t)stream, &launches);
+      const nf4_status s = launch_batch(buf, nbuf, out, lut, (cudaStream_t)stream, &launches);
       if (s != NF4_OK) return s;
       nbuf = 0;
     }
   }
   if (nbuf > 0) {
-    const nf4_status s = launch_batch(buf, nbuf, out_dtype == NF4_BF16, (cudaStream_t)stream, &launches);
+    const nf4_status s = launch_batch(buf, nbuf, out, lut, (cudaStream_t)stream, &launches);
     if (s != NF4_OK) return s;
   }
   set_launch_count(launches);
   return NF4_OK;
 }
 
-extern "C" nf4_status nf4_dequantize(const uint8_t* packed, const float* absmax, const nf4_dq_state* dq,
-                                     int64_t n, int32_t blocksize, nf4_dtype out_dtype, void* out,
-                                     void* stream) {
+extern "C" nf4_status nf4_dequantize_batched(const nf4_tensor* tensors, int32_t count, nf4_dtype out_dtype,
+                                             void* stream) {
+  if (out_dtype != NF4_F16 && out_dtype != NF4_BF16) return NF4_ERR_BAD_DTYPE;
+  return nf4_dequantize_batched_ex(tensors, count, nullptr, out_dtype, stream);
+}
+
+extern "C" nf4_status nf4_dequantize_ex(const uint8_t* packed, const float* absmax, const nf4_dq_state* dq,
+                                        int64_t n, int32_t blocksize, const float* codebook16, nf4_dtype out_dtype,
+                                        void* out, void* stream) {
   if ((absmax == nullptr) == (dq == nullptr)) return NF4_ERR_BAD_STATE;
   nf4_tensor t;
   t.packed = packed;
@@ -503,7 +553,23 @@ extern "C" nf4_status nf4_dequantize(const uint8_t* packed, const float* absmax,
   t.blocksize = blocksize;
   t.reserved = 0;
   t.out = out;
-  return nf4_dequantize_batched(&t, 1, out_dtype, stream);
+  return nf4_dequantize_batched_ex(&t, 1, codebook16, out_dtype, stream);
+}
+
+extern "C" nf4_status nf4_dequantize(const uint8_t* packed, const float* absmax, const nf4_dq_state* dq,
+                                     int64_t n, int32_t blocksize, nf4_dtype out_dtype, void* out,
+                                     void* stream) {
+  if (out_dtype != NF4_F16 && out_dtype != NF4_BF16) return NF4_ERR_BAD_DTYPE;
+  return nf4_dequantize_ex(packed, absmax, dq, n, blocksize, nullptr, out_dtype, out, stream);
+}
+
+extern "C" void nf4_codebook_fp4(float out16[16]) {
+  // BitsAndBytes FP4 (sign, 2-bit exponent, 1-bit mantissa) levels / 12 ([ext])
+  static const float v[8] = {0.0f, 0.0625f, 8.0f, 12.0f, 4.0f, 6.0f, 2.0f, 3.0f};
+  for (int i = 0; i < 8; ++i) {
+    out16[i] = v[i] / 12.0f;
+    out16[8 + i] = -(v[i] / 12.0f);
+  }
 }
 
 extern "C" void nf4_codebook(float out16[16]) {
@@ -515,7 +581,7 @@ extern "C" void nf4_codebook(float out16[16]) {
 }
 
 extern "C" int32_t nf4_dequant_grid(int64_t tiles) {
-  return grid_for(current_variant(), tiles < 1 ? 1 : tiles, false);
+  return grid_for(current_variant(), tiles < 1 ? 1 : tiles, 0);
 }
 extern "C" int64_t nf4_dequant_tile_elems(void) { return tile_elems(current_variant()); }
 extern "C" int32_t nf4_kernel_variant_count(void) { return kNumVariants; }

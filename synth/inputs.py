@@ -125,6 +125,15 @@ def dynamic_map_code2() -> np.ndarray:
     return np.sort(np.array(data, dtype=np.float32))
 
 
+def bnb_fp4_codebook() -> np.ndarray:
+    """BitsAndBytes' 16-entry FP4 table ([ext]: bnb get_4bit_type('fp4'): sign, 2-bit
+    exponent, 1-bit mantissa values {0, 0.0625, 8, 12, 4, 6, 2, 3} and negatives,
+    divided by their max).  An INPUT to nf4_dequantize_ex."""
+    data = np.array([0, 0.0625, 8.0, 12.0, 4.0, 6.0, 2.0, 3.0,
+                     -0.0, -0.0625, -8.0, -12.0, -4.0, -6.0, -2.0, -3.0], np.float32)
+    return (data / np.float32(12.0)).astype(np.float32)
+
+
 def random_codes(n_bytes: int, seed: int) -> np.ndarray:
     rng = np.random.Generator(np.random.Philox(seed))
     return rng.integers(0, 256, n_bytes, dtype=np.uint8)

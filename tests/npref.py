@@ -27,8 +27,8 @@ def to16(p: np.ndarray, dtype: str) -> np.ndarray:
 
 
 def dequant_np(packed, n, bs, dtype, absmax=None, qabsmax=None, code2=None, absmax2=None,
-               offset=0.0, bs2=256):
-    cb = NF4_DECIMAL.astype(np.float32)
+               offset=0.0, bs2=256, codebook=None):
+    cb = NF4_DECIMAL.astype(np.float32) if codebook is None else np.asarray(codebook, np.float32)
     k = np.arange(n, dtype=np.int64)
     byte = packed[k >> 1]
     idx = np.where(k % 2 == 0, byte >> 4, byte & 0x0F)
@@ -39,6 +39,8 @@ def dequant_np(packed, n, bs, dtype, absmax=None, qabsmax=None, code2=None, absm
         t = (code2[qabsmax[b]] * absmax2[b // bs2]).astype(np.float32)
         a = (t + np.float32(offset)).astype(np.float32)
     p = (cb[idx] * a).astype(np.float32)
+    if dtype == "f32":
+        return p.view(np.uint32)
     return to16(p, dtype)
 
 

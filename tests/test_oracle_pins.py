@@ -461,3 +461,53 @@ def test_double_quantize_zero_group(orc):
     absmax = np.full(300, 0.25, np.float32)
     q, a2 = orc.double_quantize(absmax, 0.25, code2, 256)
     assert (a2 == 0).all() and (code2[q] == 0).all()
+
+
+# --------------------------------------------------------------------------
+# other 16-entry codebooks and fp32 output
+# --------------------------------------------------------------------------
+def test_explicit_nf4_codebook_is_default(orc):
+    packed = syn.random_codes(5000, 1)
+    absmax = syn.hash_absmax(2, 0, 10000 // 64 + 1)
+    a = orc.dequantize(packed, 10000, 64, orc.OUT_BF16, absmax=absmax)
+    b = orc.dequantize(packed, 10000, 64, orc.OUT_BF16, absmax=absmax, codebook=orc.codebook())
+    assert np.array_equal(a, b)
+
+
+def test_fp32_output_is_the_fp32_product(orc):
+    """OUT_F32 returns fl32(CB[idx] * a) itself (numpy float32 multiply), both modes."""
+    code2 = syn.dynamic_map_code2()
+    for dq in (False, True):
+        for n in (1, 2, 63, 1025, 70001):
+            packed = syn.hash_packed(n, 0, (n + 1) // 2)
+            nb = -(-n // 64)
+            kw = (dict(qabsmax=syn.hash_qabsmax(n, 0, nb), code2=code2, absmax2=syn.hash_absmax2(n, 0, -(-nb // 256)),
+                       offset=float(syn.hash_offset(n))) if dq else dict(absmax=syn.hash_absmax(n, 0, nb)))
+            got = orc.dequantize(packed, n, 64, orc.OUT_F32, **kw)
+            assert np.array_equal(got, npref.dequant_np(packed, n, 64, "f32", **kw))
+
+
+def test_fp4_table_closed_forms(orc):
+    """BNB FP4 table with absmax 1: fp32 output is the table exactly; 16-bit
+    outputs are its RNE roundings (numpy / ml_dtypes)."""
+    cb = syn.bnb_fp4_codebook()
+    assert cb[3] == 1.0 and cb[11] == -1.0 and cb[0] == 0 and np.signbit(cb[8])
+    packed = np.array([0x01, 0x23, 0x45, 0x67, 0x89, 0xAB, 0xCD, 0xEF], np.uint8)
+    one = np.array([1.0], np.float32)
+    f32 = orc.dequantize(packed, 16, 64, orc.OUT_F32, absmax=one, codebook=cb)
+    assert np.array_equal(f32, cb.view(np.uint32))
+    for dt, code in (("f16", orc.OUT_F16), ("bf16", orc.OUT_BF16)):
+        got = orc.dequantize(packed, 16, 64, code, absmax=one, codebook=cb)
+        assert np.array_equal(got, npref.to16(cb, dt))
+
+
+@pytest.mark.parametrize("dtype", ["f16", "bf16", "f32"])
+def test_custom_codebook_bruteforce(orc, dtype):
+    rng = np.random.Generator(np.random.Philox(9))
+    cb = rng.standard_normal(16).astype(np.float32)
+    code = {"f16": orc.OUT_F16, "bf16": orc.OUT_BF16, "f32": orc.OUT_F32}[dtype]
+    for n in (1, 17, 1000, 4097):
+        packed = syn.hash_packed(n + 5, 0, (n + 1) // 2)
+        absmax = syn.hash_absmax(n + 5, 0, -(-n // 128))
+        got = orc.dequantize(packed, n, 128, code, absmax=absmax, codebook=cb)
+        assert np.array_equal(got, npref.dequant_np(packed, n, 128, dtype, absmax=absmax, codebook=cb))

@@ -380,3 +380,45 @@ def test_sol_stream(nf4):
     d = dst.cpu().numpy().view(np.uint32).reshape(-1, 4)
     x = ((s * 0x00010001) & 0xFFFFFFFF).astype(np.uint32)
     assert np.array_equal(d, np.stack([x, x, x, x], 1))
+
+
+# ---------------------------------------------------------------------------
+# other 16-entry codebooks, fp32 output
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("dtype", ["f16", "bf16", "f32"])
+@pytest.mark.parametrize("book", ["fp4", "custom"])
+def test_codebook_ex_parity(nf4, orc, dtype, book):
+    import torch
+    cb = (np.array(nf4.nf4_codebook_fp4(), np.float32) if book == "fp4"
+          else np.random.Generator(np.random.Philox(4)).standard_normal(16).astype(np.float32))
+    if book == "fp4":
+        assert np.array_equal(cb, syn.bnb_fp4_codebook())
+    code = {"f16": orc.OUT_F16, "bf16": orc.OUT_BF16, "f32": orc.OUT_F32}[dtype]
+    for dq in (False, True):
+        for n in (1, 77, 3 * TILE + 999, 10 * TILE):
+            packed, kw = _inputs(n, 64, dq, n * 3 + 1)
+            if dq:
+                d = nf4.DQ(dev(kw["qabsmax"]), dev(kw["code2"]), dev(kw["absmax2"]), kw["offset"])
+                out = nf4.nf4_dequantize_ex(dev(packed), None, d, n=n, blocksize=64, codebook=cb, out_dtype=dtype)
+            else:
+                out = nf4.nf4_dequantize_ex(dev(packed), dev(kw["absmax"]), None, n=n, blocksize=64, codebook=cb,
+                                            out_dtype=dtype)
+            torch.cuda.synchronize()
+            got = out.view(torch.int32 if dtype == "f32" else torch.int16).cpu().numpy()
+            got = got.view(np.uint32 if dtype == "f32" else np.uint16)
+            ref = orc.dequantize(packed, n, 64, code, codebook=cb, threads=8, **kw)
+            assert np.array_equal(got, ref), (book, dtype, dq, n)
+
+
+def test_batched_ex_fp32_nf4(nf4, orc):
+    import torch
+    descs, refs = [], []
+    for i, n in enumerate((5 * TILE, 4097, 2 * TILE + 64)):
+        packed, kw = _inputs(n, 128, False, 50 + i)
+        out = torch.empty(n, dtype=torch.float32, device="cuda")
+        descs.append(nf4.NF4Tensor(dev(packed), n, 128, out, dev(kw["absmax"]), None))
+        refs.append(orc.dequantize(packed, n, 128, orc.OUT_F32, **kw))
+    nf4.nf4_dequantize_batched_ex(descs, None, "f32")
+    torch.cuda.synchronize()
+    for d, ref in zip(descs, refs):
+        assert np.array_equal(d.out.cpu().numpy().view(np.uint32), ref)
