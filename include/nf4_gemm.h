@@ -1,0 +1,48 @@
+/*
+ * nf4_gemm.h -- fused NF4 dequantization + tensor-core GEMM (SURVEY 8(f) row
+ * F1, the step after the hot path: dequantization is 72.4% of the quantized
+ * matmul; the paper's weights feed FP16 tensor-core GEMMs).
+ *
+ *   Y[m, n] = sum_k X[m, k] * W[n, k]        m < M, n < N, k < K
+ *
+ * where W is an NF4 weight of shape [N, K] (rows = output features, K
+ * contiguous, the flat element index of W[n, k] is n*K + k) stored exactly as
+ * nf4_dequantize consumes it, and every W[n, k] is the hot path's value
+ * RNE16(fl32(NF4[idx] * a_b)) in X's 16-bit type (bit-identical to
+ * nf4_dequantize's output; tests/test_gemm_gpu.py checks it through one-hot X).
+ * Products are exact in fp32; accumulation is fp32 on the tcgen05 tensor cores
+ * (order unspecified), so Y is within (K * 2^-23) * sum_k |X[m,k] W[n,k]| of the
+ * exact sum, plus the final rounding when y_dtype is 16-bit (F1).
+ *
+ *   x        [device] M x K, row-major, 16-byte aligned, NF4_BF16 or NF4_F16.
+ *   packed   [device] N*K/2 bytes, 16-byte aligned.
+ *   absmax / dq  as nf4_dequantize (exactly one given); blocksize in
+ *            [64, 4096], K a multiple of 64 and of blocksize.
+ *   y        [device] M x N row-major, y_dtype NF4_F16, NF4_BF16 or NF4_F32.
+ *   splits   split-K factor (<= 0: nf4_gemm_default_splits).  splits > 1 needs
+ *            a workspace of nf4_gemm_workspace_bytes(M, N, K, splits) bytes
+ *            [device, 16-byte aligned]; partial sums are reduced in split order
+ *            (deterministic for a given splits).
+ * Stream-ordered, asynchronous; status codes as nf4.h.
+ */
+#ifndef NF4_GEMM_H_
+#define NF4_GEMM_H_
+
+#include <stdint.h>
+#include "nf4.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+nf4_status nf4_gemm(const void* x, nf4_dtype x_dtype, int32_t M, const uint8_t* packed, const float* absmax,
+                    const nf4_dq_state* dq, int32_t N, int32_t K, int32_t blocksize, void* y, nf4_dtype y_dtype,
+                    int32_t splits, void* workspace, int64_t workspace_bytes, void* stream);
+
+int32_t nf4_gemm_default_splits(int32_t M, int32_t N, int32_t K);
+int64_t nf4_gemm_workspace_bytes(int32_t M, int32_t N, int32_t K, int32_t splits);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NF4_GEMM_H_ */

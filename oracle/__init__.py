@@ -179,3 +179,17 @@ def double_quantize(absmax: np.ndarray, offset: float, code2: np.ndarray, blocks
     if rc != 0:
         raise ValueError("oracle_double_quantize rejected its arguments")
     return q, a2
+
+
+def gemm_reference(x16: np.ndarray, x_dtype: int, packed, N: int, K: int, blocksize: int, **scale_kw):
+    """Reference for the fused GEMM: W = this oracle's dequantization
+    of the NF4 weight [N, K] into x's 16-bit type (bit-exact hot-path values), then
+    Y = X . W^T with numpy in fp64 (a library matmul as one step).  Returns
+    (Y fp64 [M, N], S fp64 [M, N] = sum_k |x_mk w_nk|) -- S bounds the fp32
+    accumulation error of any summation order: |Y_gpu - Y| <= K * 2^-23 * S."""
+    import ml_dtypes
+    w16 = dequantize(packed, N * K, blocksize, x_dtype, threads=8, **scale_kw)
+    np16 = np.float16 if x_dtype == OUT_F16 else ml_dtypes.bfloat16
+    w = w16.view(np16).astype(np.float64).reshape(N, K)
+    x = np.asarray(x16, np.uint16).view(np16).astype(np.float64).reshape(-1, K)
+    return x @ w.T, np.abs(x) @ np.abs(w).T

@@ -26,6 +26,7 @@ __all__ = [
     "nf4_synth_fill", "nf4_sol_stream", "nf4_set_max_ctas", "nf4_dequant_grid", "nf4_dequant_tile_elems",
     "nf4_kernel_variants", "nf4_set_kernel_variant", "nf4_get_kernel_variant",
     "nf4_dequantize_ex", "nf4_dequantize_batched_ex", "nf4_codebook_fp4",
+    "nf4_gemm", "nf4_gemm_default_splits", "nf4_gemm_workspace_bytes",
 ]
 
 
@@ -254,3 +255,39 @@ def nf4_set_kernel_variant(v) -> int:
 
 def nf4_get_kernel_variant() -> int:
     return int(load().nf4_get_kernel_variant())
+
+
+# ---------------------------------------------------------------------------
+# F1: fused NF4 dequant + tcgen05 GEMM (include/nf4_gemm.h)
+# ---------------------------------------------------------------------------
+def nf4_gemm_default_splits(M: int, N: int, K: int) -> int:
+    return int(load().nf4_gemm_default_splits(int(M), int(N), int(K)))
+
+
+def nf4_gemm_workspace_bytes(M: int, N: int, K: int, splits: int) -> int:
+    return int(load().nf4_gemm_workspace_bytes(int(M), int(N), int(K), int(splits)))
+
+
+def nf4_gemm(x, packed, absmax=None, dq: Optional[DQ] = None, *, N: int, K: int, blocksize: int = 64,
+             y=None, y_dtype="bf16", splits: int = 0, workspace=None, stream=None):
+    """Y = X . W^T with W the NF4 weight [N, K] dequantized on the fly.
+    x: CUDA tensor [M, K] bf16/fp16.  Allocates y (and the split-K workspace) with
+    torch when not given; returns y."""
+    import torch
+    M = x.shape[0] if x.dim() == 2 else x.numel() // K
+    ycode = _dtype_code(y_dtype)
+    if y is None:
+        tdt = {_lib.NF4_F16: torch.float16, _lib.NF4_BF16: torch.bfloat16, _lib.NF4_F32: torch.float32}[ycode]
+        y = torch.empty((M, N), dtype=tdt, device=x.device)
+    if splits <= 0:
+        splits = nf4_gemm_default_splits(M, N, K)
+    wbytes = nf4_gemm_workspace_bytes(M, N, K, splits)
+    if wbytes > 0 and workspace is None:
+        workspace = torch.empty(wbytes, dtype=torch.uint8, device=x.device)
+    wsize = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    dqc = dq.c() if dq is not None else None
+    st = load().nf4_gemm(_ptr(x), _dtype_code(x.dtype), int(M), _ptr(packed), _ptr(absmax),
+                         ctypes.byref(dqc) if dqc is not None else None, int(N), int(K), int(blocksize),
+                         _ptr(y), ycode, int(splits), _ptr(workspace), int(wsize), _stream(stream))
+    _lib.check(st, "nf4_gemm")
+    return y

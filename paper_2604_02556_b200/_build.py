@@ -9,9 +9,9 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libnf4.so")
-SOURCES = ["nf4_common.cu", "nf4_dequant.cu", "nf4_quantize.cu", "nf4_tools.cu"]
+SOURCES = ["nf4_common.cu", "nf4_dequant.cu", "nf4_quantize.cu", "nf4_tools.cu", "nf4_gemm.cu"]
 HEADERS = ["nf4_internal.cuh", os.path.join("..", "..", "include", "nf4.h"),
-           os.path.join("..", "..", "include", "nf4_tools.h")]
+           os.path.join("..", "..", "include", "nf4_tools.h"), os.path.join("..", "..", "include", "nf4_gemm.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 # No --use_fast_math, no -ftz=true: IEEE subnormals and RN division/multiply

@@ -25,6 +25,7 @@ EXPORTS = [
     "nf4_synth_fill", "nf4_sol_stream", "nf4_set_max_ctas", "nf4_dequant_grid", "nf4_dequant_tile_elems",
     "nf4_kernel_variant_count", "nf4_kernel_variant_name", "nf4_set_kernel_variant", "nf4_get_kernel_variant",
     "nf4_dequantize_ex", "nf4_dequantize_batched_ex", "nf4_codebook_fp4",
+    "nf4_gemm", "nf4_gemm_default_splits", "nf4_gemm_workspace_bytes",
 ]
 
 
@@ -71,6 +72,9 @@ def load() -> ctypes.CDLL:
             "nf4_double_quantize": ([P, i64, f32, P, i32, P, P, P], st),
             "nf4_codebook": ([P], None),
             "nf4_codebook_fp4": ([P], None),
+            "nf4_gemm": ([P, i32, i32, P, P, ctypes.POINTER(DQState), i32, i32, i32, P, i32, i32, P, i64, P], st),
+            "nf4_gemm_default_splits": ([i32, i32, i32], i32),
+            "nf4_gemm_workspace_bytes": ([i32, i32, i32, i32], i64),
             "nf4_dequantize_ex": ([P, P, ctypes.POINTER(DQState), i64, i32, P, i32, P, P], st),
             "nf4_dequantize_batched_ex": ([ctypes.POINTER(TensorDesc), i32, P, i32, P], st),
             "nf4_status_string": ([st], ctypes.c_char_p),

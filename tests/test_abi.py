@@ -23,7 +23,7 @@ def lib():
 
 def _declared_symbols():
     names = set()
-    for h in ("nf4.h", "nf4_tools.h"):
+    for h in ("nf4.h", "nf4_tools.h", "nf4_gemm.h"):
         src = open(os.path.join(ROOT, "include", h)).read()
         src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
         for m in re.finditer(r"\b(nf4_[a-z0-9_]+)\s*\(", src):
@@ -56,6 +56,8 @@ def test_library_is_sm100a_with_256bit_stores(lib):
     assert "STG.E.EF.ENL2.256" in sass          # 256-bit evict-first output stores
     assert "LDG.E.NA.64.CONSTANT" in sass       # non-allocating read-only code loads
     assert "FFMA" not in _kernel_sass(sass, "dequant_kernel")  # product never contracted
+    g = _kernel_sass(sass, "nf4_gemm_kernel")                   # F1: tcgen05 MMA + TMEM loads
+    assert "UTCHMMA" in g and "LDTM" in g and "FFMA" not in g
 
 
 def _kernel_sass(sass, name):

@@ -1,0 +1,125 @@
+"""F1: fused NF4 dequant + tcgen05 GEMM vs the oracle.
+
+* one-hot X rows make every Y[m, n] a single exact product 1 * W[n, k_m], so the
+  weights the tensor cores consumed are checked BIT-EXACT against the oracle's
+  dequantization (the hot path's definition);
+* random X: |Y - Y_ref| <= K * 2^-23 * sum_k |x w| (+ the output rounding for
+  16-bit Y), Y_ref in fp64 from oracle.gemm_reference.
+"""
+from __future__ import annotations
+
+import ml_dtypes
+import numpy as np
+import pytest
+
+from synth import inputs as syn
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def nf4():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2604_02556_b200 as m
+    m.load()
+    return m
+
+
+def dev(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _weights(N, K, bs, dq, seed):
+    n = N * K
+    nb = n // bs
+    packed = syn.hash_packed(seed, 0, n // 2)
+    if dq:
+        kw = dict(qabsmax=syn.hash_qabsmax(seed, 0, nb), code2=syn.dynamic_map_code2(),
+                  absmax2=syn.hash_absmax2(seed, 0, -(-nb // 256)), offset=float(syn.hash_offset(seed)))
+    else:
+        kw = dict(absmax=syn.hash_absmax(seed, 0, nb))
+    return packed, kw
+
+
+def _run(nf4, x16, xdt, M, packed, kw, N, K, bs, ydt, splits):
+    import torch
+    tdt = torch.bfloat16 if xdt == "bf16" else torch.float16
+    x = dev(x16.view(np.int16)).view(tdt).reshape(M, K)
+    if "absmax" in kw:
+        y = nf4.nf4_gemm(x, dev(packed), dev(kw["absmax"]), None, N=N, K=K, blocksize=bs, y_dtype=ydt, splits=splits)
+    else:
+        d = nf4.DQ(dev(kw["qabsmax"]), dev(kw["code2"]), dev(kw["absmax2"]), kw["offset"])
+        y = nf4.nf4_gemm(x, dev(packed), None, d, N=N, K=K, blocksize=bs, y_dtype=ydt, splits=splits)
+    torch.cuda.synchronize()
+    return y
+
+
+@pytest.mark.parametrize("xdt", ["bf16", "f16"])
+@pytest.mark.parametrize("dq", [False, True])
+def test_gemm_weights_bit_exact_via_one_hot(nf4, orc, xdt, dq):
+    """Y[m, n] = W[n, k_m] exactly: the tensor cores saw the hot path's weights."""
+    for (M, N, K, bs, splits) in ((16, 256, 512, 64, 1), (5, 384, 1024, 128, 3), (40, 200, 640, 64, 2)):
+        packed, kw = _weights(N, K, bs, dq, seed=M + N + K)
+        ks = (np.arange(M) * 37 + 11) % K
+        x = np.zeros((M, K), np.float32)
+        x[np.arange(M), ks] = 1.0
+        x16 = (x.astype(ml_dtypes.bfloat16) if xdt == "bf16" else x.astype(np.float16)).view(np.uint16)
+        y = _run(nf4, x16, xdt, M, packed, kw, N, K, bs, "f32", splits).cpu().numpy()
+        code = orc.OUT_BF16 if xdt == "bf16" else orc.OUT_F16
+        w16 = orc.dequantize(packed, N * K, bs, code, threads=8, **kw).reshape(N, K)
+        np16 = ml_dtypes.bfloat16 if xdt == "bf16" else np.float16
+        want = w16[:, ks].T.view(np16).astype(np.float32)           # [M, N]
+        assert np.array_equal(y.view(np.uint32), want.view(np.uint32)), (M, N, K)
+
+
+SHAPES = [(1, 128, 64), (2, 256, 1024), (7, 384, 2048), (16, 1024, 4096), (33, 640, 1536),
+          (64, 512, 5376), (100, 256, 1024), (130, 384, 512), (300, 256, 768)]
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES)
+def test_gemm_random_within_fp32_bound(nf4, orc, M, N, K):
+    rng = np.random.Generator(np.random.Philox(M * 1000 + K))
+    x16 = rng.standard_normal((M, K)).astype(np.float32).astype(ml_dtypes.bfloat16).view(np.uint16)
+    for dq in (False, True):
+        packed, kw = _weights(N, K, 64, dq, seed=N + K + int(dq))
+        ref, mag = orc.gemm_reference(x16, orc.OUT_BF16, packed, N, K, 64, **kw)
+        for splits in (1, 0):
+            y = _run(nf4, x16, "bf16", M, packed, kw, N, K, 64, "f32", splits).cpu().numpy().astype(np.float64)
+            bound = K * 2.0 ** -23 * mag + 1e-30
+            err = np.abs(y - ref)
+            assert (err <= bound).all(), (M, N, K, dq, splits, float((err / bound).max()))
+
+
+def test_gemm_bf16_output_rounding(nf4, orc):
+    M, N, K = 24, 384, 2048
+    rng = np.random.Generator(np.random.Philox(5))
+    x16 = rng.standard_normal((M, K)).astype(np.float32).astype(ml_dtypes.bfloat16).view(np.uint16)
+    packed, kw = _weights(N, K, 64, True, 17)
+    ref, mag = orc.gemm_reference(x16, orc.OUT_BF16, packed, N, K, 64, **kw)
+    y = _run(nf4, x16, "bf16", M, packed, kw, N, K, 64, "bf16", 0).float().cpu().numpy().astype(np.float64)
+    # fp32 accumulation bound, then one bf16 rounding (half ulp = 2^-8 relative)
+    bound = K * 2.0 ** -23 * mag * (1 + 2.0 ** -8) + np.abs(ref) * 2.0 ** -8 + 1e-30
+    assert (np.abs(y - ref) <= bound).all()
+
+
+def test_gemm_split_k_is_deterministic(nf4):
+    M, N, K = 8, 512, 8192
+    rng = np.random.Generator(np.random.Philox(8))
+    x16 = rng.standard_normal((M, K)).astype(np.float32).astype(ml_dtypes.bfloat16).view(np.uint16)
+    packed, kw = _weights(N, K, 64, True, 3)
+    a = _run(nf4, x16, "bf16", M, packed, kw, N, K, 64, "f32", 4).cpu().numpy()
+    b = _run(nf4, x16, "bf16", M, packed, kw, N, K, 64, "f32", 4).cpu().numpy()
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def test_gemm_argument_errors(nf4):
+    import torch
+    x = torch.zeros((4, 100), dtype=torch.bfloat16, device="cuda")
+    p = torch.zeros(100 * 128 // 2, dtype=torch.uint8, device="cuda")
+    a = torch.ones(200, dtype=torch.float32, device="cuda")
+    with pytest.raises(nf4.NF4Error) as e:
+        nf4.nf4_gemm(x, p, a, None, N=128, K=100)             # K not a multiple of 64
+    assert e.value.status == 2
