@@ -11,21 +11,31 @@
 // quantized matmul and the fused, preprocessing-free direction is the
 // one it leaves open.
 //
-// Roles (160 threads):
-//   warps 0-3  producers: thread t owns W row n0+t of the tile; per 64-element
-//              k-chunk it dequantizes 64 weights into a 128-byte swizzled row,
-//              and the 128 threads together copy the X tile (BN rows x 128 B);
-//              then fence.proxy.async + mbarrier arrive (full[s]).  After the K
-//              loop they are the epilogue: tcgen05.ld of their 32 TMEM lanes.
-//   warp 4     TMEM allocator and MMA issuer: waits full[s], issues 4 x
-//              tcgen05.mma (K=16 each), tcgen05.commit -> empty[s]; after the
-//              last chunk commits -> done.
+// Roles (320 threads):
+//   warp 9     TMA issuer (one lane): per 64-element k-chunk, a 2-D TMA box of
+//              the packed codes (128 rows x 32 B) and a 2-D TMA box of X
+//              (BN rows x 64 elements, SWIZZLE_128B: lands directly in the UMMA
+//              canonical layout, zero-filled past M) -> tma_full[s].
+//   warps 0-7  producers: threads 2r, 2r+1 own W row n0+r; each reads its 16
+//              code bytes from shared memory, dequantizes 32 weights into 4 of
+//              the row's 8 swizzled 16-B chunks, fence.proxy.async, arrive
+//              w_full[s].  After the K loop they are the epilogue: warp w reads
+//              TMEM lanes 32(w%4).. and column half w/4 with tcgen05.ld.
+//   warp 8     TMEM allocator and MMA issuer: waits tma_full[s] + w_full[s],
+//              issues 4 x tcgen05.mma (K=16 each), tcgen05.commit -> empty[s];
+//              after the last chunk commits -> done.
+// (A first version had every producer thread load its own row's codes: row-
+// strided 16-B loads cost 32 L1 wavefronts per warp instruction and capped the
+// kernel at ~0.5 TB/s; TMA boxes fetch the same bytes with full-line requests.)
 // Swap-AB orientation: the MMA's M=128 side is the weight (128 output
 // features), its N side the tokens (BN in {16,...,256}), so decode-size M
 // wastes nothing.  Split-K over gridDim.z writes fp32 partials to a caller
 // workspace; nf4_gemm_reduce sums them in split order (deterministic).
+#include <cuda.h>  // CUtensorMap (the encoder is fetched at run time; no libcuda link)
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <mutex>
 
 #include "nf4_internal.cuh"
 #include "../../include/nf4_gemm.h"
@@ -33,8 +43,10 @@
 namespace nf4 {
 namespace gemm {
 
-constexpr int kProducers = 128;
-constexpr int kThreads = kProducers + 32;
+constexpr int kProducers = 256;             // 2 threads per weight row (32 elements each)
+constexpr int kProducerWarps = kProducers / 32;
+constexpr int kThreads = kProducers + 64;   // + MMA warp + TMA warp
+constexpr int kCodeBytes = 32;              // packed bytes per row per k-chunk
 constexpr int kChunk = 64;          // k elements per stage (= one 128 B swizzle row in 16-bit)
 constexpr int kRowBytes = 128;
 
@@ -71,9 +83,9 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity)
   while (!done) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.b32 %0, 1, 0, p;\n\t}"
-        : "=r"(done) : "r"(b), "r"(parity) : "memory");
+        : "=r"(done) : "r"(b), "r"(parity), "r"(0x989680) : "memory");
   }
 }
 
@@ -90,21 +102,28 @@ __device__ __forceinline__ uint32_t umma_idesc(int n, bool bf16) {
   return (1u << 4) | (fmt << 7) | (fmt << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(128 >> 4) << 24);
 }
 
-__device__ __forceinline__ float dq_scale(const GemmParams& p, const float* code2s, int64_t b) {
-  if (p.absmax != nullptr) return __ldg(p.absmax + b);
-  const uint32_t q = __ldg(p.qabsmax + b);
-  return __fadd_rn(__fmul_rn(code2s[q], __ldg(p.absmax2 + (b >> 8))), p.offset);
+__device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
 }
 
 template <int BN, int STAGES, int RING, bool BF16>
-__global__ void __launch_bounds__(kThreads, 1) nf4_gemm_kernel(const __grid_constant__ GemmParams p) {
+__global__ void __launch_bounds__(kThreads, 1)
+    nf4_gemm_kernel(const __grid_constant__ GemmParams p, const __grid_constant__ CUtensorMap map_codes,
+                    const __grid_constant__ CUtensorMap map_x) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // 1024-B alignment for the swizzle atoms
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* smem_w = smem;                                     // STAGES x 16 KB
-  uint8_t* smem_x = smem_w + STAGES * 128 * kRowBytes;        // STAGES x BN x 128 B
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_x + STAGES * BN * kRowBytes);
-  uint64_t* empty = full + STAGES;
+  // 1024-B alignment for the swizzle atoms (offset arithmetic on the __shared__
+  // array keeps the shared address space visible to the compiler: LDS/STS)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* smem_w = smem;                                     // STAGES x 16 KB  (bf16 W, SW128)
+  uint8_t* smem_x = smem_w + STAGES * 128 * kRowBytes;        // STAGES x BN x 128 B (X, SW128, by TMA)
+  uint8_t* smem_c = smem_x + STAGES * BN * kRowBytes;         // STAGES x 4 KB (packed codes, by TMA)
+  uint64_t* tma_full = reinterpret_cast<uint64_t*>(smem_c + STAGES * 128 * kCodeBytes);
+  uint64_t* w_full = tma_full + STAGES;
+  uint64_t* empty = w_full + STAGES;
   uint64_t* done = empty + STAGES;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(done + 1);
   float* lut = reinterpret_cast<float*>(tmem_holder + 4);
@@ -119,6 +138,7 @@ __global__ void __launch_bounds__(kThreads, 1) nf4_gemm_kernel(const __grid_cons
   const int kc1 = min(nk_total, kc0 + p.chunks_per_split);
   const int nk = kc1 > kc0 ? kc1 - kc0 : 0;
   constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
+  constexpr uint32_t kStageTx = 128 * kCodeBytes + BN * kRowBytes;
 
   if (threadIdx.x < 16) lut[threadIdx.x] = p.lut[threadIdx.x];
   if (p.absmax == nullptr) {
@@ -126,64 +146,50 @@ __global__ void __launch_bounds__(kThreads, 1) nf4_gemm_kernel(const __grid_cons
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], kProducers);
+      mbar_init(&tma_full[s], 1);
+      mbar_init(&w_full[s], kProducers);
       mbar_init(&empty[s], 1);
     }
     mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 4) {
+  if (warp == kProducerWarps) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
                  "n"(TMEM_COLS) : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (warp == kProducerWarps + 1 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_codes)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_x)) : "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_holder;
 
-  if (warp < 4) {
-    // ======================= producers =======================
-    // Register ring of depth RING: the global loads (32 B of codes, the
-    // block-scale inputs, this thread's share of the X tile) of chunk i+RING
-    // are issued before chunk i is dequantized, so each thread keeps RING
-    // chunks (128 B of codes at RING = 4) in flight.
-    const int t = threadIdx.x;
+  if (warp < kProducerWarps) {
+    // ======================= producers (dequantize) =======================
+    // The block-scale inputs of chunk i+RING are loaded while chunk i is
+    // dequantized (register ring); the codes arrive by TMA.
+    const int t = threadIdx.x >> 1;            // tile row
+    const int half = threadIdx.x & 1;          // elements 32*half .. 32*half+31 of the chunk
     const int row = n0 + t;                    // weight row (output feature)
     const bool row_ok = row < p.N;
-    const int64_t row_base = int64_t(row) * p.K;
-    constexpr int XCH = BN * 8 / kProducers > 0 ? BN * 8 / kProducers : 1;  // 16-B X chunks per thread
-    uint4 rc0[RING], rc1[RING];
+    const int64_t blk_base = (int64_t(row) * p.K) >> p.bs_shift;
+    const int chunk_shift = p.bs_shift - 6;    // 64-element chunks per quantization block = 2^chunk_shift
     uint32_t rq[RING];     // fp32 absmax bits, or qabsmax (DQ)
     float ra2[RING];       // absmax2 (DQ)
-    uint4 rx[RING][XCH];
     auto issue = [&](int d, int i) {
-      const int k0 = (kc0 + i) * kChunk;
-      rc0[d] = make_uint4(0, 0, 0, 0);
-      rc1[d] = make_uint4(0, 0, 0, 0);
       rq[d] = 0;
       ra2[d] = 0.0f;
       if (row_ok) {
-        const uint8_t* cp = p.packed + ((row_base + k0) >> 1);
-        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(rc0[d].x), "=r"(rc0[d].y), "=r"(rc0[d].z), "=r"(rc0[d].w) : "l"(cp));
-        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(rc1[d].x), "=r"(rc1[d].y), "=r"(rc1[d].z), "=r"(rc1[d].w) : "l"(cp + 16));
-        const int64_t b = (row_base + k0) >> p.bs_shift;
+        const int64_t b = blk_base + ((kc0 + i) >> chunk_shift);
         if (p.absmax != nullptr) {
           rq[d] = __float_as_uint(__ldg(p.absmax + b));
         } else {
           rq[d] = __ldg(p.qabsmax + b);
           ra2[d] = __ldg(p.absmax2 + (b >> 8));
         }
-      }
-#pragma unroll
-      for (int j = 0; j < XCH; ++j) {
-        const int idx = t + j * kProducers;
-        const int m = idx >> 3, c = idx & 7;
-        rx[d][j] = make_uint4(0, 0, 0, 0);
-        if (idx < BN * 8 && m0 + m < p.M)
-          rx[d][j] = __ldg(reinterpret_cast<const uint4*>(p.x + int64_t(m0 + m) * p.K + k0 + c * 8));
       }
     };
 #pragma unroll
@@ -198,44 +204,43 @@ __global__ void __launch_bounds__(kThreads, 1) nf4_gemm_kernel(const __grid_cons
         // block scale (A4): fp32 absmax, or fl32(fl32(code2[q] * absmax2) + offset)
         const float a = p.absmax != nullptr ? __uint_as_float(rq[d])
                                             : __fadd_rn(__fmul_rn(code2s[rq[d]], ra2[d]), p.offset);
-        mbar_wait_parity(&empty[s], ((i / STAGES) & 1) ^ 1);
-        // dequantize 64 weights of this row -> 8 swizzled 16-B chunks
+        if (i + RING < nk) issue(d, i + RING);
+        mbar_wait_parity(&tma_full[s], (i / STAGES) & 1);   // codes (and X) landed; W[s] is free
+        const uint4 c0 = *reinterpret_cast<const uint4*>(smem_c + s * 128 * kCodeBytes + t * kCodeBytes + 16 * half);
+        // dequantize 32 weights of this row -> 4 swizzled 16-B chunks
         uint8_t* wrow = smem_w + s * 128 * kRowBytes + t * kRowBytes;
-        const uint32_t cw[8] = {rc0[d].x, rc0[d].y, rc0[d].z, rc0[d].w, rc1[d].x, rc1[d].y, rc1[d].z, rc1[d].w};
+        const uint32_t cw[4] = {c0.x, c0.y, c0.z, c0.w};
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {     // chunk c = elements 8c..8c+7 = code bytes 4c..4c+3
-          const uint32_t x = cw[c];
+        for (int cc = 0; cc < 4; ++cc) {  // chunk c = elements 8c..8c+7 = code bytes 4c..4c+3
+          const int c = 4 * half + cc;
+          const uint32_t x = cw[cc];
+          const uint32_t hi4 = (x >> 2) & 0x3C3C3C3Cu;  // byte j = 4 * high nibble (LUT byte offset)
+          const uint32_t lo4 = (x << 2) & 0x3C3C3C3Cu;  // byte j = 4 * low nibble
           uint32_t w4[4];
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            const uint32_t byte = (x >> (8 * j)) & 0xFFu;
-            const float ph2 = __fmul_rn(lut[byte >> 4], a);
-            const float pl2 = __fmul_rn(lut[byte & 0x0Fu], a);
+            const uint32_t oh = j == 0 ? (hi4 & 0xFFu) : j == 3 ? (hi4 >> 24) : __byte_perm(hi4, 0u, 0x4440u + j);
+            const uint32_t ol = j == 0 ? (lo4 & 0xFFu) : j == 3 ? (lo4 >> 24) : __byte_perm(lo4, 0u, 0x4440u + j);
+            const float ph2 = __fmul_rn(*reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(lut) + oh), a);
+            const float pl2 = __fmul_rn(*reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(lut) + ol), a);
             w4[j] = pack2_rn<BF16>(ph2, pl2);
           }
           *reinterpret_cast<uint4*>(wrow + ((c ^ (t & 7)) << 4)) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
         }
-        uint8_t* xs = smem_x + s * BN * kRowBytes;
-#pragma unroll
-        for (int j = 0; j < XCH; ++j) {
-          const int idx = t + j * kProducers;
-          if (idx < BN * 8) {
-            const int m = idx >> 3, c = idx & 7;
-            *reinterpret_cast<uint4*>(xs + m * kRowBytes + ((c ^ (m & 7)) << 4)) = rx[d][j];
-          }
-        }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive(&full[s]);
-        if (i + RING < nk) issue(d, i + RING);
+        mbar_arrive(&w_full[s]);
       }
     }
     // ======================= epilogue =======================
     mbar_wait_parity(done, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int n = n0 + warp * 32 + lane;
-    const uint32_t taddr = tmem + (uint32_t(warp * 32) << 16);
+    const int q = warp & 3;                          // TMEM lane quarter this warp may access
+    constexpr int HB = BN / 2 < 16 ? 16 : BN / 2;    // columns per warp (BN = 16: warps 4-7 idle)
+    const int col0 = (warp >> 2) * HB;
+    const int n = n0 + q * 32 + lane;
+    const uint32_t taddr = tmem + (uint32_t(q * 32) << 16);
 #pragma unroll
-    for (int cb = 0; cb < BN; cb += 16) {
+    for (int cb = col0; cb < col0 + HB && cb < BN; cb += 16) {
       uint32_t v[16];
       asm volatile(
           "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
@@ -261,12 +266,26 @@ __global__ void __launch_bounds__(kThreads, 1) nf4_gemm_kernel(const __grid_cons
         }
       }
     }
+  } else if (warp == kProducerWarps + 1) {
+    // ======================= TMA issuer (one thread) =======================
+    if (lane == 0) {
+      for (int i = 0; i < nk; ++i) {
+        const int s = i % STAGES;
+        mbar_wait_parity(&empty[s], ((i / STAGES) & 1) ^ 1);   // MMA of chunk i-STAGES released the slot
+        const int k0 = (kc0 + i) * kChunk;
+        asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
+            smem_u32(&tma_full[s])), "r"(kStageTx) : "memory");
+        tma_load_2d(smem_c + s * 128 * kCodeBytes, &map_codes, k0 / 2, n0, &tma_full[s]);
+        tma_load_2d(smem_x + s * BN * kRowBytes, &map_x, k0, m0, &tma_full[s]);
+      }
+    }
   } else if (lane == 0) {
     // ======================= MMA issuer (one thread) =======================
     const uint32_t idesc = umma_idesc(BN, BF16);
     for (int i = 0; i < nk; ++i) {
       const int s = i % STAGES;
-      mbar_wait_parity(&full[s], (i / STAGES) & 1);
+      mbar_wait_parity(&tma_full[s], (i / STAGES) & 1);
+      mbar_wait_parity(&w_full[s], (i / STAGES) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t wa = smem_u32(smem_w + s * 128 * kRowBytes);
       const uint32_t xa = smem_u32(smem_x + s * BN * kRowBytes);
@@ -292,7 +311,7 @@ __global__ void __launch_bounds__(kThreads, 1) nf4_gemm_kernel(const __grid_cons
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 4) {
+  if (warp == kProducerWarps) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS) : "memory");
   }
@@ -313,7 +332,7 @@ __global__ void nf4_gemm_reduce_kernel(const float* __restrict__ partial, int sp
 
 template <int BN>
 constexpr int stages_for() {
-  return BN <= 128 ? 4 : 3;
+  return BN <= 32 ? 3 : BN <= 128 ? 4 : 3;   // BN <= 32: 66 KB -> 3 CTAs per SM
 }
 template <int BN>
 constexpr int ring_for() {
@@ -322,18 +341,50 @@ constexpr int ring_for() {
 
 template <int BN>
 constexpr size_t smem_bytes() {
-  return 1024 /*align slack*/ + size_t(stages_for<BN>()) * (128 + BN) * kRowBytes + 2 * 8 * 8 + 64 + 64 + 1024 + 64;
+  return 1024 /*align slack*/ + size_t(stages_for<BN>()) * ((128 + BN) * kRowBytes + 128 * kCodeBytes) +
+         (3 * stages_for<BN>() + 1) * 8 + 16 + 64 + 1024 + 64;
 }
 
 template <int BN, bool BF16>
-static cudaError_t launch(const GemmParams& p, dim3 grid, cudaStream_t s) {
+static cudaError_t launch(const GemmParams& p, const CUtensorMap& mc, const CUtensorMap& mx, dim3 grid,
+                          cudaStream_t s) {
   constexpr int ST = stages_for<BN>();
   auto k = nf4_gemm_kernel<BN, ST, ring_for<BN>(), BF16>;
   constexpr size_t sm = smem_bytes<BN>();
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
   if (e != cudaSuccess) return e;
-  k<<<grid, kThreads, sm, s>>>(p);
+  k<<<grid, kThreads, sm, s>>>(p, mc, mx);
   return cudaPeekAtLastError();
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encoder() {
+  static std::once_flag once;
+  static EncodeTiledFn fn = nullptr;
+  std::call_once(once, [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(f);
+  });
+  return fn;
+}
+
+// 2-D tensor map over a row-major [rows, cols] matrix of `elem` bytes.
+static bool make_map(CUtensorMap* m, CUtensorMapDataType dt, int elem, const void* base, uint64_t cols,
+                     uint64_t rows, uint32_t box_cols, uint32_t box_rows, CUtensorMapSwizzle sw) {
+  EncodeTiledFn enc = encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {cols * uint64_t(elem)};
+  const cuuint32_t box[2] = {box_cols, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace gemm
@@ -355,16 +406,49 @@ extern "C" int64_t nf4_gemm_workspace_bytes(int32_t M, int32_t N, int32_t K, int
   return int64_t(splits) * M * N * 4;
 }
 
+template <int BN, bool BF16>
+static int gemm_occupancy() {
+  static int occ = 0;
+  if (occ == 0) {
+    int v = 0;
+    auto k = nf4_gemm_kernel<BN, stages_for<BN>(), ring_for<BN>(), BF16>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_bytes<BN>()));
+    occ = (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, kThreads, smem_bytes<BN>()) == cudaSuccess && v > 0)
+              ? v : 1;
+  }
+  return occ;
+}
+
+static int occupancy_for_bn(int bn) {
+  switch (bn) {
+    case 16: return gemm_occupancy<16, true>();
+    case 32: return gemm_occupancy<32, true>();
+    case 64: return gemm_occupancy<64, true>();
+    case 128: return gemm_occupancy<128, true>();
+    default: return gemm_occupancy<256, true>();
+  }
+}
+
+// Split-K factor minimising the makespan of the (row tile, token tile, split)
+// grid on this GPU: waves x (chunks per split + ~2 chunks of per-CTA prologue
+// and epilogue), preferring fewer splits on near ties (less partial traffic).
 extern "C" int32_t nf4_gemm_default_splits(int32_t M, int32_t N, int32_t K) {
   if (M <= 0 || N <= 0 || K <= 0) return 1;
   const int bn = pick_bn(M);
   const int64_t tiles = int64_t((N + 127) / 128) * ((M + bn - 1) / bn);
-  const int64_t target = int64_t(sm_count()) * 2;  // ~2 CTAs per SM
-  int64_t s = (target + tiles - 1) / tiles;
+  const int64_t cap = int64_t(sm_count()) * occupancy_for_bn(bn);
   const int64_t nk = K / 64;
-  if (s > nk / 4) s = nk / 4 > 0 ? nk / 4 : 1;      // keep >= 4 chunks per split
-  if (s > 32) s = 32;
-  return int32_t(s < 1 ? 1 : s);
+  int best_s = 1;
+  double best = 1e30;
+  for (int64_t sp = 1; sp <= 32 && sp <= nk; ++sp) {
+    const int64_t waves = (tiles * sp + cap - 1) / cap;
+    const double cost = double(waves) * double((nk + sp - 1) / sp + 2);
+    if (cost < best * 0.97) {
+      best = cost;
+      best_s = int(sp);
+    }
+  }
+  return best_s;
 }
 
 extern "C" nf4_status nf4_gemm(const void* x, nf4_dtype x_dtype, int32_t M, const uint8_t* packed,
@@ -414,13 +498,19 @@ extern "C" nf4_status nf4_gemm(const void* x, nf4_dtype x_dtype, int32_t M, cons
   dim3 grid((N + 127) / 128, (M + bn - 1) / bn, splits);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool bf16 = x_dtype == NF4_BF16;
+  CUtensorMap mc, mx;
+  if (!make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, packed, uint64_t(K) / 2, uint64_t(N), kCodeBytes, 128,
+                CU_TENSOR_MAP_SWIZZLE_NONE) ||
+      !make_map(&mx, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, x, uint64_t(K),
+                uint64_t(M), kChunk, uint32_t(bn), CU_TENSOR_MAP_SWIZZLE_128B))
+    return NF4_ERR_CUDA;
   cudaError_t e;
   switch (bn) {
-    case 16: e = bf16 ? launch<16, true>(p, grid, s) : launch<16, false>(p, grid, s); break;
-    case 32: e = bf16 ? launch<32, true>(p, grid, s) : launch<32, false>(p, grid, s); break;
-    case 64: e = bf16 ? launch<64, true>(p, grid, s) : launch<64, false>(p, grid, s); break;
-    case 128: e = bf16 ? launch<128, true>(p, grid, s) : launch<128, false>(p, grid, s); break;
-    default: e = bf16 ? launch<256, true>(p, grid, s) : launch<256, false>(p, grid, s); break;
+    case 16: e = bf16 ? launch<16, true>(p, mc, mx, grid, s) : launch<16, false>(p, mc, mx, grid, s); break;
+    case 32: e = bf16 ? launch<32, true>(p, mc, mx, grid, s) : launch<32, false>(p, mc, mx, grid, s); break;
+    case 64: e = bf16 ? launch<64, true>(p, mc, mx, grid, s) : launch<64, false>(p, mc, mx, grid, s); break;
+    case 128: e = bf16 ? launch<128, true>(p, mc, mx, grid, s) : launch<128, false>(p, mc, mx, grid, s); break;
+    default: e = bf16 ? launch<256, true>(p, mc, mx, grid, s) : launch<256, false>(p, mc, mx, grid, s); break;
   }
   if (e != cudaSuccess) { cudaGetLastError(); return NF4_ERR_CUDA; }
   int launches = 1;
