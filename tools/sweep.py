@@ -1,0 +1,100 @@
+#!/usr/bin/env python
+"""BASELINE config 5 sweep: blocksize 64/128/256/4096 x fp16/bf16 x n = 2^20..2^30
+(fp32 absmax primary; --dq for double-quant), 1 GPU, single-tensor nf4_dequantize.
+
+Each point: W warm-up launches, then K timed launches with CUDA events; inputs
+smaller than ~4x L2 are timed with an L2 flush (a 256 MB write) between launches
+and reported as "cold"; larger ones need no flush.  Prints a markdown table and
+writes JSON lines to --out.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    import torch
+
+    import paper_2604_02556_b200 as nf4
+    from paper_2604_02556_b200 import _lib
+    from synth import workloads as wl
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--dq", action="store_true")
+    ap.add_argument("--min-log2", type=int, default=20)
+    ap.add_argument("--max-log2", type=int, default=30)
+    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args()
+    torch.cuda.set_device(0)
+    nf4.load()
+    # L2 flush by READING 512 MB (a write-based flush leaves 256 MB of dirty lines whose
+    # lazy write-back would then be charged to the timed launch)
+    flush = torch.ones(512 << 20, dtype=torch.uint8, device="cuda")
+    sink = torch.empty(1, dtype=torch.int64, device="cuda")
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+    nmax = 1 << args.max_log2
+    packed = torch.empty(nmax // 2, dtype=torch.uint8, device="cuda")
+    nf4.nf4_synth_fill(_lib.NF4_SYNTH_CODES, 5, 0, nmax // 2, packed)
+    out = torch.empty(nmax, dtype=torch.int16, device="cuda")
+    rows = []
+    print("| bs | dtype | n | cold/hot | us | GB/s | % of measured copy | Gelem/s |")
+    print("|---|---|---|---|---|---|---|---|")
+    for bs in (64, 128, 256, 4096):
+        nb = nmax // bs
+        if args.dq:
+            q = torch.empty(nb, dtype=torch.uint8, device="cuda")
+            nf4.nf4_synth_fill(_lib.NF4_SYNTH_QABSMAX, 6, 0, nb, q)
+            a2 = torch.empty(-(-nb // 256), dtype=torch.float32, device="cuda")
+            nf4.nf4_synth_fill(_lib.NF4_SYNTH_ABSMAX2, 6, 0, a2.numel(), a2)
+            from synth import inputs as syn
+            code2 = torch.from_numpy(syn.dynamic_map_code2()).cuda()
+            dq = nf4.DQ(q, code2, a2, 0.05)
+            absmax = None
+        else:
+            absmax = torch.empty(nb, dtype=torch.float32, device="cuda")
+            nf4.nf4_synth_fill(_lib.NF4_SYNTH_ABSMAX, 6, 0, nb, absmax)
+            dq = None
+        for dt in ("f16", "bf16"):
+            for lg in range(args.min_log2, args.max_log2 + 1):
+                n = 1 << lg
+                cold = n * 2.5 < 4 * 126e6
+                f = lambda: nf4.nf4_dequantize(packed, absmax, dq, n=n, blocksize=bs, out_dtype=dt, out=out)
+                for _ in range(3):
+                    f()
+                torch.cuda.synchronize()
+                times = []
+                for _ in range(args.reps):
+                    if cold:
+                        torch.sum(flush, dtype=torch.int64, out=sink)
+                    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    s.record()
+                    f()
+                    e.record()
+                    torch.cuda.synchronize()
+                    times.append(s.elapsed_time(e))
+                times.sort()
+                ms = times[len(times) // 2]
+                alg = n * wl.algorithmic_bytes_per_element(bs, args.dq)
+                gbs = alg / (ms * 1e-3) / 1e9
+                r = {"blocksize": bs, "dtype": dt, "n": n, "dq": args.dq, "cold": cold, "us": round(ms * 1e3, 2),
+                     "gbs": round(gbs, 1), "frac_measured_copy": round(gbs / peak, 4),
+                     "gelem_s": round(n / (ms * 1e-3) / 1e9, 1)}
+                rows.append(r)
+                print(f"| {bs} | {dt} | 2^{lg} | {'cold' if cold else 'hot'} | {r['us']} | {r['gbs']} | "
+                      f"{100 * r['frac_measured_copy']:.1f}% | {r['gelem_s']} |", flush=True)
+    if args.out:
+        with open(args.out, "w") as fo:
+            for r in rows:
+                fo.write(json.dumps(r) + "\n")
+
+
+if __name__ == "__main__":
+    main()
