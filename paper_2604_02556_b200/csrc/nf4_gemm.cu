@@ -110,6 +110,14 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* m
       : "memory");
 }
 
+// TMEM column budget: the fp32 accumulator (BN columns) at column 0, then
+// STAGES dequantized A tiles of 32 columns (128 lanes x 64 16-bit weights).
+template <int BN, int STAGES>
+__host__ __device__ constexpr int tmem_cols() {
+  constexpr int need = (BN < 32 ? 32 : BN) + STAGES * 32;
+  return need <= 32 ? 32 : need <= 64 ? 64 : need <= 128 ? 128 : need <= 256 ? 256 : 512;
+}
+
 template <int BN, int STAGES, int RING, bool BF16>
 __global__ void __launch_bounds__(kThreads, 1)
     nf4_gemm_kernel(const __grid_constant__ GemmParams p, const __grid_constant__ CUtensorMap map_codes,
@@ -118,8 +126,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // 1024-B alignment for the swizzle atoms (offset arithmetic on the __shared__
   // array keeps the shared address space visible to the compiler: LDS/STS)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* smem_w = smem;                                     // STAGES x 16 KB  (bf16 W, SW128)
-  uint8_t* smem_x = smem_w + STAGES * 128 * kRowBytes;        // STAGES x BN x 128 B (X, SW128, by TMA)
+  uint8_t* smem_x = smem;                                     // STAGES x BN x 128 B (X, SW128, by TMA)
   uint8_t* smem_c = smem_x + STAGES * BN * kRowBytes;         // STAGES x 4 KB (packed codes, by TMA)
   uint64_t* tma_full = reinterpret_cast<uint64_t*>(smem_c + STAGES * 128 * kCodeBytes);
   uint64_t* w_full = tma_full + STAGES;
@@ -137,7 +144,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int kc0 = split * p.chunks_per_split;
   const int kc1 = min(nk_total, kc0 + p.chunks_per_split);
   const int nk = kc1 > kc0 ? kc1 - kc0 : 0;
-  constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
+  constexpr int TMEM_COLS = tmem_cols<BN, STAGES>();
+  constexpr int ACC_COLS = BN < 32 ? 32 : BN;                 // A stages start here (32-column aligned)
   constexpr uint32_t kStageTx = 128 * kCodeBytes + BN * kRowBytes;
 
   if (threadIdx.x < 16) lut[threadIdx.x] = p.lut[threadIdx.x];
@@ -168,15 +176,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_holder;
 
   if (warp < kProducerWarps) {
-    // ======================= producers (dequantize) =======================
-    // The block-scale inputs of chunk i+RING are loaded while chunk i is
-    // dequantized (register ring); the codes arrive by TMA.
-    const int t = threadIdx.x >> 1;            // tile row
-    const int half = threadIdx.x & 1;          // elements 32*half .. 32*half+31 of the chunk
+    // ======================= producers (dequantize into TMEM) =======================
+    // Warp w may only address TMEM lanes 32(w%4)..32(w%4)+31, so thread (w, l)
+    // owns weight row r = 32(w%4)+l of the tile and k-half h = w/4 (32 of the
+    // chunk's 64 elements).  The block-scale inputs of chunk i+RING are loaded
+    // while chunk i is dequantized (register ring); the codes arrive by TMA.
+    const int t = 32 * (warp & 3) + lane;      // tile row = TMEM lane
+    const int half = warp >> 2;
     const int row = n0 + t;                    // weight row (output feature)
     const bool row_ok = row < p.N;
     const int64_t blk_base = (int64_t(row) * p.K) >> p.bs_shift;
     const int chunk_shift = p.bs_shift - 6;    // 64-element chunks per quantization block = 2^chunk_shift
+    const uint32_t tlane = uint32_t(32 * (warp & 3)) << 16;
     uint32_t rq[RING];     // fp32 absmax bits, or qabsmax (DQ)
     float ra2[RING];       // absmax2 (DQ)
     auto issue = [&](int d, int i) {
@@ -205,29 +216,34 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float a = p.absmax != nullptr ? __uint_as_float(rq[d])
                                             : __fadd_rn(__fmul_rn(code2s[rq[d]], ra2[d]), p.offset);
         if (i + RING < nk) issue(d, i + RING);
-        mbar_wait_parity(&tma_full[s], (i / STAGES) & 1);   // codes (and X) landed; W[s] is free
+        mbar_wait_parity(&tma_full[s], (i / STAGES) & 1);   // codes (and X) landed; A stage s is free
         const uint4 c0 = *reinterpret_cast<const uint4*>(smem_c + s * 128 * kCodeBytes + t * kCodeBytes + 16 * half);
-        // dequantize 32 weights of this row -> 4 swizzled 16-B chunks
-        uint8_t* wrow = smem_w + s * 128 * kRowBytes + t * kRowBytes;
+        // dequantize 32 weights: word j = (element 2j) | (element 2j+1) << 16
         const uint32_t cw[4] = {c0.x, c0.y, c0.z, c0.w};
+        uint32_t w[16];
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {  // chunk c = elements 8c..8c+7 = code bytes 4c..4c+3
-          const int c = 4 * half + cc;
+        for (int cc = 0; cc < 4; ++cc) {
           const uint32_t x = cw[cc];
           const uint32_t hi4 = (x >> 2) & 0x3C3C3C3Cu;  // byte j = 4 * high nibble (LUT byte offset)
           const uint32_t lo4 = (x << 2) & 0x3C3C3C3Cu;  // byte j = 4 * low nibble
-          uint32_t w4[4];
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const uint32_t oh = j == 0 ? (hi4 & 0xFFu) : j == 3 ? (hi4 >> 24) : __byte_perm(hi4, 0u, 0x4440u + j);
             const uint32_t ol = j == 0 ? (lo4 & 0xFFu) : j == 3 ? (lo4 >> 24) : __byte_perm(lo4, 0u, 0x4440u + j);
             const float ph2 = __fmul_rn(*reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(lut) + oh), a);
             const float pl2 = __fmul_rn(*reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(lut) + ol), a);
-            w4[j] = pack2_rn<BF16>(ph2, pl2);
+            w[4 * cc + j] = pack2_rn<BF16>(ph2, pl2);
           }
-          *reinterpret_cast<uint4*>(wrow + ((c ^ (t & 7)) << 4)) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        // 16 columns (32 weights) of this row's A tile in TMEM
+        const uint32_t taddr = tmem + tlane + uint32_t(ACC_COLS + s * 32 + half * 16);
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+            ::"r"(taddr), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]),
+            "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]), "r"(w[15])
+            : "memory");
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         mbar_arrive(&w_full[s]);
       }
     }
@@ -287,18 +303,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait_parity(&tma_full[s], (i / STAGES) & 1);
       mbar_wait_parity(&w_full[s], (i / STAGES) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t wa = smem_u32(smem_w + s * 128 * kRowBytes);
       const uint32_t xa = smem_u32(smem_x + s * BN * kRowBytes);
 #pragma unroll
       for (int kk = 0; kk < kChunk / 16; ++kk) {
-        const uint64_t adesc = umma_desc_sw128(wa + kk * 32);
+        const uint32_t a_tmem = tmem + uint32_t(ACC_COLS + s * 32 + kk * 8);   // A: 128 lanes x 16 weights
         const uint64_t bdesc = umma_desc_sw128(xa + kk * 32);
         const uint32_t accum = (i > 0 || kk > 0) ? 1u : 0u;
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
             "setp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
-            ::"r"(tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum) : "memory");
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}"
+            ::"r"(tmem), "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accum) : "memory");
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
           smem_u32(&empty[s])) : "memory");
@@ -332,7 +347,8 @@ __global__ void nf4_gemm_reduce_kernel(const float* __restrict__ partial, int sp
 
 template <int BN>
 constexpr int stages_for() {
-  return BN <= 32 ? 3 : BN <= 128 ? 4 : 3;   // BN <= 32: 66 KB -> 3 CTAs per SM
+  // TMEM: accumulator + STAGES x 32 columns; BN <= 32 -> 128 columns -> 4 CTAs/SM fit in 512
+  return BN <= 32 ? 3 : BN <= 64 ? 6 : BN <= 128 ? 4 : 5;
 }
 template <int BN>
 constexpr int ring_for() {
@@ -341,7 +357,7 @@ constexpr int ring_for() {
 
 template <int BN>
 constexpr size_t smem_bytes() {
-  return 1024 /*align slack*/ + size_t(stages_for<BN>()) * ((128 + BN) * kRowBytes + 128 * kCodeBytes) +
+  return 1024 /*align slack*/ + size_t(stages_for<BN>()) * (BN * kRowBytes + 128 * kCodeBytes) +
          (3 * stages_for<BN>() + 1) * 8 + 16 + 64 + 1024 + 64;
 }
 
