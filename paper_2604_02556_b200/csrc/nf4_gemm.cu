@@ -133,8 +133,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = w_full + STAGES;
   uint64_t* done = empty + STAGES;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(done + 1);
-  float* lut = reinterpret_cast<float*>(tmem_holder + 4);
-  float* code2s = lut + 16;                                   // 256 floats (DQ)
+  __shared__ __align__(256) float lut[16];                    // 256-B aligned: address = PRMT(offsets, base)
+  __shared__ float code2s[256];                               // DQ second-level table
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * 128;
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&tma_full[s], 1);
-      mbar_init(&w_full[s], kProducers);
+      mbar_init(&w_full[s], kProducerWarps);   // one elected arrive per producer warp
       mbar_init(&empty[s], 1);
     }
     mbar_init(done, 1);
@@ -188,6 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int64_t blk_base = (int64_t(row) * p.K) >> p.bs_shift;
     const int chunk_shift = p.bs_shift - 6;    // 64-element chunks per quantization block = 2^chunk_shift
     const uint32_t tlane = uint32_t(32 * (warp & 3)) << 16;
+    const uint32_t lut_base = smem_u32(lut);   // low byte 0: PRMT splices a byte offset into it
     uint32_t rq[RING];     // fp32 absmax bits, or qabsmax (DQ)
     float ra2[RING];       // absmax2 (DQ)
     auto issue = [&](int d, int i) {
@@ -228,11 +229,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t lo4 = (x << 2) & 0x3C3C3C3Cu;  // byte j = 4 * low nibble
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            const uint32_t oh = j == 0 ? (hi4 & 0xFFu) : j == 3 ? (hi4 >> 24) : __byte_perm(hi4, 0u, 0x4440u + j);
-            const uint32_t ol = j == 0 ? (lo4 & 0xFFu) : j == 3 ? (lo4 >> 24) : __byte_perm(lo4, 0u, 0x4440u + j);
-            const float ph2 = __fmul_rn(*reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(lut) + oh), a);
-            const float pl2 = __fmul_rn(*reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(lut) + ol), a);
-            w[4 * cc + j] = pack2_rn<BF16>(ph2, pl2);
+            // shared address of NF4[idx] = lut_base with byte 0 replaced by byte j of hi4/lo4: one PRMT
+            const uint32_t ah = __byte_perm(hi4, lut_base, 0x7650u + j);
+            const uint32_t al = __byte_perm(lo4, lut_base, 0x7650u + j);
+            float ch, cl;
+            asm("ld.shared.f32 %0, [%1];" : "=f"(ch) : "r"(ah));
+            asm("ld.shared.f32 %0, [%1];" : "=f"(cl) : "r"(al));
+            w[4 * cc + j] = pack2_rn<BF16>(__fmul_rn(ch, a), __fmul_rn(cl, a));
           }
         }
         // 16 columns (32 weights) of this row's A tile in TMEM
@@ -244,7 +247,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             : "memory");
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        mbar_arrive(&w_full[s]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&w_full[s]);
       }
     }
     // ======================= epilogue =======================
