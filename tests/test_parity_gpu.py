@@ -422,3 +422,32 @@ def test_batched_ex_fp32_nf4(nf4, orc):
     torch.cuda.synchronize()
     for d, ref in zip(descs, refs):
         assert np.array_equal(d.out.cpu().numpy().view(np.uint32), ref)
+
+
+def test_batched_dequant_captured_in_cuda_graph(nf4, orc):
+    """The batched path is graph-capturable (no host syncs, no allocations): a
+    whole 'model' step captured once and replayed gives the oracle's bytes."""
+    import torch
+    descs, refs = [], []
+    for i, n in enumerate((7 * TILE, 3 * TILE + 5, 1000, 12 * TILE)):
+        packed, kw = _inputs(n, 64, bool(i % 2), 200 + i)
+        out = torch.zeros(n, dtype=torch.bfloat16, device="cuda")
+        if "absmax" in kw:
+            descs.append(nf4.NF4Tensor(dev(packed), n, 64, out, dev(kw["absmax"]), None))
+        else:
+            descs.append(nf4.NF4Tensor(dev(packed), n, 64, out, None,
+                                       nf4.DQ(dev(kw["qabsmax"]), dev(kw["code2"]), dev(kw["absmax2"]), kw["offset"])))
+        refs.append(_oracle(orc, packed, kw, n, 64, "bf16"))
+    s = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        nf4.nf4_dequantize_batched(descs, "bf16", stream=s)
+    for d in descs:
+        d.out.zero_()
+    torch.cuda.synchronize()
+    g.replay()
+    g.replay()
+    torch.cuda.synchronize()
+    for d, ref in zip(descs, refs):
+        assert np.array_equal(host16(d.out), ref)

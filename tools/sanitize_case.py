@@ -1,0 +1,77 @@
+#!/usr/bin/env python
+"""Small workload for compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
+every kernel of libnf4 on tiny, ragged and unaligned inputs.  Exits non-zero on a
+parity mismatch so the sanitizer run also checks results.
+
+    compute-sanitizer --tool memcheck --error-exitcode 9 python tools/sanitize_case.py
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    import numpy as np
+    import torch
+
+    import oracle
+    import paper_2604_02556_b200 as nf4
+    from paper_2604_02556_b200 import _lib
+    from synth import inputs as syn
+
+    torch.cuda.set_device(0)
+    d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    bad = 0
+    code2 = syn.dynamic_map_code2()
+    variants = nf4.nf4_kernel_variants()
+    only_default = os.environ.get("NF4_SANITIZE_DEFAULT_ONLY") == "1"
+    for v in ([nf4.nf4_get_kernel_variant()] if only_default else range(len(variants))):
+        nf4.nf4_set_kernel_variant(v)
+        for n in (1, 31, 16384 + 77, 3 * 16384):
+            for dq in (False, True):
+                nb = -(-n // 64)
+                packed = syn.hash_packed(n, 0, (n + 1) // 2)
+                if dq:
+                    kw = dict(qabsmax=syn.hash_qabsmax(n, 0, nb), code2=code2,
+                              absmax2=syn.hash_absmax2(n, 0, -(-nb // 256)), offset=float(syn.hash_offset(n)))
+                    out = nf4.nf4_dequantize(d(packed), None, nf4.DQ(d(kw["qabsmax"]), d(code2), d(kw["absmax2"]),
+                                                                   kw["offset"]), n=n, blocksize=64, out_dtype="bf16")
+                else:
+                    kw = dict(absmax=syn.hash_absmax(n, 0, nb))
+                    out = nf4.nf4_dequantize(d(packed), d(kw["absmax"]), None, n=n, blocksize=64, out_dtype="bf16")
+                torch.cuda.synchronize()
+                ref = oracle.dequantize(packed, n, 64, oracle.OUT_BF16, **kw)
+                bad += int(not np.array_equal(out.view(torch.int16).cpu().numpy().view(np.uint16), ref))
+    # unaligned output
+    n = 5000
+    packed = syn.hash_packed(3, 0, n // 2)
+    am = syn.hash_absmax(3, 0, -(-n // 64))
+    buf = torch.zeros(n + 8, dtype=torch.int16, device="cuda")
+    nf4.nf4_dequantize(d(packed), d(am), None, n=n, blocksize=64, out_dtype="f16", out=buf[1:1 + n].view(torch.float16))
+    # quantizers
+    w = syn.gaussian_weights(4097, 1)
+    p, a = nf4.nf4_quantize(d(w), 64)
+    q = nf4.nf4_double_quantize(a, 0.05, d(code2))
+    # fused GEMM (both split modes), tiny
+    x = torch.randn(3, 256, device="cuda").to(torch.bfloat16)
+    wp = d(syn.hash_packed(9, 0, 128 * 256 // 2))
+    wa = d(syn.hash_absmax(9, 0, 128 * 256 // 64))
+    for s in (1, 2):
+        nf4.nf4_gemm(x, wp, wa, None, N=128, K=256, splits=s)
+    # synth + sol
+    buf8 = torch.empty(8192 * 4, dtype=torch.uint8, device="cuda")
+    nf4.nf4_synth_fill(_lib.NF4_SYNTH_CODES, 1, 3, 1000, buf8)
+    nf4.nf4_synth_fill(_lib.NF4_SYNTH_CODES, 1, 0, buf8.numel(), buf8)
+    dst = torch.empty(8192 * 16, dtype=torch.uint8, device="cuda")
+    nf4.nf4_sol_stream(buf8, 8192 * 4, dst)
+    torch.cuda.synchronize()
+    print("sanitize_case: parity mismatches =", bad)
+    sys.exit(1 if bad else 0)
+
+
+if __name__ == "__main__":
+    main()
