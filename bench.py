@@ -215,7 +215,7 @@ def measure_sol(nf4, torch, in_bytes=2 << 30, reps=10):
     return round(5 * in_bytes / (ms * 1e-3) / 1e9, 1)
 
 
-def run_e2e(nf4, torch, ws, args, max_host_bytes):
+def run_e2e(nf4, torch, ws, args, max_host_bytes, device=None, world=1):
     """Same metric through nf4_dequantize_host: pinned host inputs -> HBM ->
     kernel -> pinned host outputs, copies inside the timed region."""
     c = wl.CONFIGS[args.config]
@@ -262,15 +262,22 @@ def run_e2e(nf4, torch, ws, args, max_host_bytes):
     for _ in range(2):
         step()
     k = args.e2e_steps
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(k):
-        step()
+        step()                       # synchronous: returns with the outputs on the host
     dt = (time.perf_counter() - t0) / k
     del wsp
-    return {"value": round(alg / dt / 1e9, 2), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h), "ms_per_step": round(dt * 1e3, 2),
-            "gelem_per_s": round(sum(it[3] for it in items) / dt / 1e9, 3),
+    # whole job: max time over ranks, summed work (the ranks stream concurrently)
+    dt_ms, alg_all, elems_all = reduce_over_ranks(dt * 1e3, float(alg), float(sum(it[3] for it in items)),
+                                                  device if device is not None else "cpu", world)
+    dt = dt_ms * 1e-3
+    return {"value": round(alg_all / dt / 1e9, 2), "unit": UNIT, "h2d_bytes_per_step": int(h2d) * world,
+            "d2h_bytes_per_step": int(d2h) * world, "ms_per_step": round(dt * 1e3, 2),
+            "gelem_per_s": round(elems_all / dt / 1e9, 3),
             "sample": f"first {len(chosen)} of {len(ws.entries)} tensors "
                       f"({sum(it[3] for it in items) / 1e9:.2f} G elements) through nf4_dequantize_host, "
                       f"pinned host buffers, {chunk}-element chunks"}
@@ -404,11 +411,7 @@ def run_ours(args, rank, world, local_rank):
         except Exception:
             avail = 16 << 30
         budget = int(min(avail // (4 * max(world, 1)), args.e2e_host_gb * (1 << 30)))
-        e2e = run_e2e(nf4, torch, ws, args, budget)
-        if world > 1:
-            v = torch.tensor([e2e["value"]], dtype=torch.float64, device=device)
-            dist.all_reduce(v, op=dist.ReduceOp.SUM)  # independent per-rank pipelines; aggregate GB/s
-            e2e["value"] = round(float(v.item()), 2)
+        e2e = run_e2e(nf4, torch, ws, args, budget, device=device, world=world)
 
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -1,8 +1,6 @@
 cd $GRAFT_REPO_ROOT
-mkdir -p gpurun_out
-python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -1
-for tool in initcheck; do
-  echo "== $tool"
-  NF4_SANITIZE_DEFAULT_ONLY=1 timeout 900 /usr/local/cuda/bin/compute-sanitizer --tool $tool --error-exitcode 9 python tools/sanitize_case.py > gpurun_out/sanitize_$tool.txt 2>&1
-  echo "rc=$?"; tail -3 gpurun_out/sanitize_$tool.txt
-done
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" 2>&1 | tail -1
+timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+timeout 300 python tools/gemm_probe.py 16 21504 5376
+for m in 1 16 64; do timeout 300 python tools/gemm_bench.py --m $m --layers 8 --steps 10 --no-unfused 2>&1 | tail -1; done
+timeout 600 python bench.py --steps 100 --no-e2e --no-cpu-baseline 2>/dev/null | python -c "import json,sys;d=json.loads(sys.stdin.read());print(d['value'], d['roofline']['achieved'], d['roofline']['frac'], d['clocks'])"

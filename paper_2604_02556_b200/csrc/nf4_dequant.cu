@@ -153,6 +153,7 @@ template <int OUT, int VEC, bool PRMT>
 __device__ __forceinline__ void decode_group(const float* lut, const CodeVec<VEC>& q, float a,
                                              uint32_t (&w)[OutWords<OUT, VEC>::value]) {
   if constexpr (PRMT) {
+    const uint64_t aa = f32x2_splat(a);
 #pragma unroll
     for (int i = 0; i < VEC / 4; ++i) {
       const uint32_t x = q.w[i];
@@ -162,8 +163,8 @@ __device__ __forceinline__ void decode_group(const float* lut, const CodeVec<VEC
       for (int k = 0; k < 4; ++k) {
         const uint32_t oh = k == 0 ? (hi4 & 0xFFu) : k == 3 ? (hi4 >> 24) : __byte_perm(hi4, 0u, 0x4440u + k);
         const uint32_t ol = k == 0 ? (lo4 & 0xFFu) : k == 3 ? (lo4 >> 24) : __byte_perm(lo4, 0u, 0x4440u + k);
-        const float ph = __fmul_rn(lut_at(lut, oh), a);  // element 2j
-        const float pl = __fmul_rn(lut_at(lut, ol), a);  // element 2j+1
+        float ph = lut_at(lut, oh), pl = lut_at(lut, ol);  // elements 2j, 2j+1
+        mul2_rn(ph, pl, aa);                               // fl32(NF4[idx] * a), one FMUL2
         put_pair<OUT, VEC>(w, 4 * i + k, ph, pl);
       }
     }

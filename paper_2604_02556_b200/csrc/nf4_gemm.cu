@@ -221,6 +221,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint4 c0 = *reinterpret_cast<const uint4*>(smem_c + s * 128 * kCodeBytes + t * kCodeBytes + 16 * half);
         // dequantize 32 weights: word j = (element 2j) | (element 2j+1) << 16
         const uint32_t cw[4] = {c0.x, c0.y, c0.z, c0.w};
+        const uint64_t aa = f32x2_splat(a);
         uint32_t w[16];
 #pragma unroll
         for (int cc = 0; cc < 4; ++cc) {
@@ -235,7 +236,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             float ch, cl;
             asm("ld.shared.f32 %0, [%1];" : "=f"(ch) : "r"(ah));
             asm("ld.shared.f32 %0, [%1];" : "=f"(cl) : "r"(al));
-            w[4 * cc + j] = pack2_rn<BF16>(__fmul_rn(ch, a), __fmul_rn(cl, a));
+            mul2_rn(ch, cl, aa);                      // fl32(NF4[idx] * a) for both, one FMUL2
+            w[4 * cc + j] = pack2_rn<BF16>(ch, cl);
           }
         }
         // 16 columns (32 weights) of this row's A tile in TMEM

@@ -67,6 +67,21 @@ __device__ __forceinline__ uint32_t pack2_rn(float lo, float hi) {
   return r;
 }
 
+// Two IEEE round-to-nearest fp32 products in one instruction (sm_100 FMUL2,
+// PTX mul.rn.f32x2, no FTZ): x *= a, y *= a with `aa` = {a, a} packed.  Each lane
+// is exactly __fmul_rn, so the result is bit-identical to two FMULs.
+__device__ __forceinline__ uint64_t f32x2_splat(float a) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(r) : "f"(a));
+  return r;
+}
+__device__ __forceinline__ void mul2_rn(float& x, float& y, uint64_t aa) {
+  uint64_t v, r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(v) : "f"(x), "f"(y));
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(v), "l"(aa));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(r));
+}
+
 template <bool BF16>
 __device__ __forceinline__ uint16_t cvt1_rn(float x) {
   uint16_t r;
