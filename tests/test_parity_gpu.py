@@ -451,3 +451,28 @@ def test_batched_dequant_captured_in_cuda_graph(nf4, orc):
     torch.cuda.synchronize()
     for d, ref in zip(descs, refs):
         assert np.array_equal(host16(d.out), ref)
+
+
+def test_single_tensor_beyond_2_pow_32_elements(nf4, orc):
+    """64-bit indexing: one tensor of 2^32 + 4160 elements (ragged tail); sampled
+    blocks around 2^31, 2^32 and the tail are checked against the oracle."""
+    import torch
+    from paper_2604_02556_b200 import _lib
+    n = (1 << 32) + 4160
+    bs = 64
+    nb = -(-n // bs)
+    seed = 77
+    packed = torch.empty((n + 1) // 2, dtype=torch.uint8, device="cuda")
+    nf4.nf4_synth_fill(_lib.NF4_SYNTH_CODES, seed, 0, packed.numel(), packed)
+    absmax = torch.empty(nb, dtype=torch.float32, device="cuda")
+    nf4.nf4_synth_fill(_lib.NF4_SYNTH_ABSMAX, seed, 0, nb, absmax)
+    out = torch.empty(n, dtype=torch.int16, device="cuda")
+    nf4.nf4_dequantize(packed, absmax, None, n=n, blocksize=bs, out_dtype="bf16", out=out.view(torch.bfloat16))
+    torch.cuda.synchronize()
+    for b in (0, (1 << 31) // bs - 1, (1 << 31) // bs, (1 << 32) // bs - 1, (1 << 32) // bs, nb - 2, nb - 1):
+        k0, k1 = b * bs, min(n, (b + 1) * bs)
+        ref = orc.dequantize(syn.hash_packed(seed, k0 // 2, (k1 - k0 + 1) // 2), k1 - k0, bs, orc.OUT_BF16,
+                             absmax=syn.hash_absmax(seed, b, 1))
+        assert np.array_equal(out[k0:k1].cpu().numpy().view(np.uint16), ref), b
+    del packed, absmax, out
+    torch.cuda.empty_cache()
