@@ -1,0 +1,106 @@
+"""NF4Linear: a drop-in quantized linear layer on top of the C-ABI (the paper's
+"standard quantized linear layer API", re-built B200-native).
+
+The weight [out_features, in_features] is stored as BNB-format NF4 codes with
+blockwise absmax (double-quantized by default, QLoRA's format).  forward():
+
+* decode-size inputs (M = tokens <= ``fused_max_m``) run the fused NF4 dequant +
+  tcgen05 GEMM (``nf4_gemm``): the 16-bit weight never exists in HBM;
+* larger M (prefill) dequantize once with ``nf4_dequantize`` into a reusable
+  buffer and use a library GEMM (cuBLAS via torch.matmul).
+
+Both paths use exactly the hot path's weight values (bit-exact to the oracle).
+"""
+from __future__ import annotations
+
+from typing import Optional
+
+import torch
+
+from . import DQ, nf4_dequantize, nf4_double_quantize, nf4_gemm, nf4_quantize
+
+
+class NF4Linear(torch.nn.Module):
+    def __init__(self, in_features: int, out_features: int, blocksize: int = 64, double_quant: bool = True,
+                 compute_dtype: torch.dtype = torch.bfloat16, device=None, fused_max_m: int = 128):
+        super().__init__()
+        if compute_dtype not in (torch.bfloat16, torch.float16):
+            raise ValueError("compute_dtype must be bfloat16 or float16")
+        self.in_features, self.out_features = in_features, out_features
+        self.blocksize, self.double_quant = blocksize, double_quant
+        self.compute_dtype = compute_dtype
+        self.fused_max_m = fused_max_m
+        n = in_features * out_features
+        nb = -(-n // blocksize)
+        dev = torch.device(device) if device is not None else torch.device("cuda")
+        self.register_buffer("packed", torch.zeros((n + 1) // 2, dtype=torch.uint8, device=dev))
+        if double_quant:
+            self.register_buffer("qabsmax", torch.zeros(nb, dtype=torch.uint8, device=dev))
+            self.register_buffer("absmax2", torch.zeros(-(-nb // 256), dtype=torch.float32, device=dev))
+            self.register_buffer("code2", torch.zeros(256, dtype=torch.float32, device=dev))
+            self.offset = 0.0
+            self.absmax = None
+        else:
+            self.register_buffer("absmax", torch.zeros(nb, dtype=torch.float32, device=dev))
+        self.bias: Optional[torch.Tensor] = None
+        self._wbuf: Optional[torch.Tensor] = None
+
+    # ------------------------------------------------------------------ build
+    @classmethod
+    def from_weight(cls, weight: torch.Tensor, bias: Optional[torch.Tensor] = None, blocksize: int = 64,
+                    double_quant: bool = True, compute_dtype: torch.dtype = torch.bfloat16,
+                    code2: Optional[torch.Tensor] = None, fused_max_m: int = 128) -> "NF4Linear":
+        """Quantize a dense [out, in] weight on the GPU (nf4_quantize, + nf4_double_quantize
+        with offset = mean(absmax) and the BNB signed dynamic code table by default)."""
+        out_f, in_f = weight.shape
+        m = cls(in_f, out_f, blocksize, double_quant, compute_dtype, weight.device, fused_max_m)
+        w = weight.detach().contiguous()
+        if w.dtype not in (torch.float32, torch.float16, torch.bfloat16):
+            w = w.float()
+        if double_quant:
+            absmax = torch.empty(m.qabsmax.numel(), dtype=torch.float32, device=w.device)
+            nf4_quantize(w.reshape(-1), blocksize, packed=m.packed, absmax=absmax)
+            if code2 is None:
+                from synth import inputs as syn  # the BNB table is plain data (an input)
+                code2 = torch.from_numpy(syn.dynamic_map_code2())
+            m.code2.copy_(code2.to(device=w.device, dtype=torch.float32))
+            m.offset = float(absmax.double().mean().item())
+            nf4_double_quantize(absmax, m.offset, m.code2, qabsmax=m.qabsmax, absmax2=m.absmax2)
+        else:
+            nf4_quantize(w.reshape(-1), blocksize, packed=m.packed, absmax=m.absmax)
+        if bias is not None:
+            m.bias = bias.detach().to(compute_dtype).clone()
+        return m
+
+    def _dq(self) -> Optional[DQ]:
+        return DQ(self.qabsmax, self.code2, self.absmax2, self.offset) if self.double_quant else None
+
+    # --------------------------------------------------------------- compute
+    def dequantize(self, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """The dense weight [out, in] in compute_dtype (the hot path, bit-exact)."""
+        n = self.in_features * self.out_features
+        w = nf4_dequantize(self.packed, self.absmax, self._dq(), n=n, blocksize=self.blocksize,
+                           out_dtype=self.compute_dtype, out=out)
+        return w.view(self.out_features, self.in_features)
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        shape = x.shape
+        x2 = x.reshape(-1, self.in_features).to(self.compute_dtype).contiguous()
+        M, K = x2.shape
+        fused_ok = (K % 64 == 0 and K % self.blocksize == 0 and x2.data_ptr() % 16 == 0
+                    and self.packed.data_ptr() % 16 == 0)
+        if M <= self.fused_max_m and fused_ok:
+            y = nf4_gemm(x2, self.packed, self.absmax, self._dq(), N=self.out_features, K=K,
+                         blocksize=self.blocksize, y_dtype=self.compute_dtype)
+        else:
+            if self._wbuf is None or self._wbuf.numel() != self.in_features * self.out_features:
+                self._wbuf = torch.empty(self.in_features * self.out_features, dtype=self.compute_dtype,
+                                         device=x.device)
+            y = x2 @ self.dequantize(self._wbuf).t()
+        if self.bias is not None:
+            y = y + self.bias
+        return y.reshape(*shape[:-1], self.out_features)
+
+    def extra_repr(self) -> str:
+        return (f"in_features={self.in_features}, out_features={self.out_features}, blocksize={self.blocksize}, "
+                f"double_quant={self.double_quant}, compute_dtype={self.compute_dtype}")
