@@ -134,25 +134,54 @@ def oracle_sample_inputs(cfg, n):
     return packed, kw
 
 
-def time_oracle(cfg, target_s=10.0, max_elems=None, threads=None):
+_SAMPLE_CACHE = {}
+
+
+def _sample(cfg, n):
+    """Counter-based inputs for a sample of n elements, generated once per (cfg, n)."""
+    key = (cfg, n)
+    if key not in _SAMPLE_CACHE:
+        _SAMPLE_CACHE.clear()
+        _SAMPLE_CACHE[key] = oracle_sample_inputs(cfg, n)
+    return _SAMPLE_CACHE[key]
+
+
+def size_oracle_sample(cfg, target_s, threads):
+    """Elements the oracle processes in ~target_s seconds on `threads` threads."""
+    import oracle
+    c = wl.CONFIGS[cfg]
+    code = oracle.OUT_F16 if c.out_dtype == "f16" else oracle.OUT_BF16
+    probe_n = 1 << 25   # 64 MB of output: larger than the host caches, like the sample
+    packed, kw = oracle_sample_inputs(cfg, probe_n)
+    oracle.dequantize(packed, 1 << 20, c.blocksize, code, threads=threads, **kw)   # load + warm up
+    t0 = time.perf_counter()
+    oracle.dequantize(packed, probe_n, c.blocksize, code, threads=threads, **kw)
+    rate = probe_n / max(time.perf_counter() - t0, 1e-6)
+    n = max(1 << 22, min(int(rate * target_s), 1 << 31))
+    return n - n % 16384
+
+
+def time_oracle(cfg, target_s=10.0, threads=None, n=None):
     """Time the oracle (as it stands) on this host's cores over a bounded sample
-    of the workload sized to ~target_s seconds.  Returns a cpu_baseline dict."""
+    of the workload (~target_s seconds, or exactly n elements).  Returns a
+    cpu_baseline dict."""
     import oracle
     c = wl.CONFIGS[cfg]
     threads = threads or len(os.sched_getaffinity(0))
     code = oracle.OUT_F16 if c.out_dtype == "f16" else oracle.OUT_BF16
-    probe_n = 1 << 22
-    packed, kw = oracle_sample_inputs(cfg, probe_n)
-    t0 = time.perf_counter()
-    oracle.dequantize(packed, probe_n, c.blocksize, code, threads=threads, **kw)
-    rate = probe_n / max(time.perf_counter() - t0, 1e-6)
-    n = int(rate * target_s)
-    n = max(1 << 22, min(n, max_elems or (1 << 31)))
-    n -= n % 16384
-    packed, kw = oracle_sample_inputs(cfg, n)
-    t0 = time.perf_counter()
-    oracle.dequantize(packed, n, c.blocksize, code, threads=threads, **kw)
-    dt = time.perf_counter() - t0
+    resize = n is None
+    if n is None:
+        n = size_oracle_sample(cfg, target_s, threads)
+    while True:
+        packed, kw = _sample(cfg, n)
+        t0 = time.perf_counter()
+        oracle.dequantize(packed, n, c.blocksize, code, threads=threads, **kw)
+        dt = time.perf_counter() - t0
+        if not resize or dt >= 0.5 * target_s or n >= 1 << 31:
+            break
+        resize = False                      # one re-size from a full-size run
+        n = int(min(1 << 31, n * target_s / max(dt, 1e-3)))
+        n -= n % 16384
     bpe = wl.algorithmic_bytes_per_element(c.blocksize, c.dq)
     return {"value": round(n * bpe / dt / 1e9, 3), "unit": UNIT, "cores": threads, "kind": "oracle",
             "gelem_per_s": round(n / dt / 1e9, 4), "seconds": round(dt, 2),
@@ -165,9 +194,16 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     cfg = args.config
+    # each step is a bounded sample sized so the whole run takes ~90 s
+    per_step = args.ref_step_seconds or max(0.2, min(5.0, 90.0 / max(1, args.steps + args.warmup)))
+    threads = len(os.sched_getaffinity(0))
+    n = size_oracle_sample(cfg, per_step, threads)
+    first = time_oracle(cfg, threads=threads, n=n)          # re-size once from a full-size run
+    n = int(min(1 << 31, max(1 << 22, n * per_step / max(first["seconds"], 1e-3))))
+    n -= n % 16384
     steps = []
     for i in range(args.warmup + args.steps):
-        cb = time_oracle(cfg, target_s=args.ref_step_seconds)
+        cb = time_oracle(cfg, threads=threads, n=n)
         if i >= args.warmup:
             steps.append(cb)
     v = statistics.median(s["value"] for s in steps)
@@ -469,7 +505,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sol", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    ap.add_argument("--ref-step-seconds", type=float, default=5.0)
+    ap.add_argument("--ref-step-seconds", type=float, default=None,
+                    help="oracle seconds per reference step (default: ~90 s / (steps + warmup), 0.2..5 s)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-host-gb", type=float, default=4.0)
     args = ap.parse_args()
