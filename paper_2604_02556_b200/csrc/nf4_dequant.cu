@@ -88,13 +88,18 @@ struct TensorDesc {
   int32_t pad_;
 };
 
-struct BatchParams {
+// Kernel parameters (passed by value, __grid_constant__).  MAXB sizes the
+// descriptor array: 1 and 16 keep single-tensor / per-layer launches light
+// (the parameter block is copied at every launch), 128 is the batched maximum.
+template <int MAXB>
+struct BatchParamsT {
   int64_t total_tiles;
   int32_t count;
   int32_t pad_;
   float lut[16];          // the 16-entry codebook (NF4 unless nf4_dequantize_ex supplies one)
-  TensorDesc t[NF4_MAX_BATCH];
+  TensorDesc t[MAXB];
 };
+using BatchParams = BatchParamsT<NF4_MAX_BATCH>;
 
 // Per-block absmax decode (A4).  fp32: absmax[b].  DQ (R7):
 // fl32(fl32(code2[q] * absmax2[b >> 8]) + offset), two roundings, no FMA.
@@ -247,8 +252,9 @@ __device__ __forceinline__ int64_t clc_result(const uint4* result) {
   return ok ? int64_t(x) : -1;
 }
 
-template <int OUT, int VEC, int U, bool PERSIST, bool SSCALE, bool PRMT, bool CLC, bool DB = false>
-__global__ void __launch_bounds__(kThreads) dequant_kernel(const __grid_constant__ BatchParams P) {
+template <int OUT, int VEC, int U, bool PERSIST, bool SSCALE, bool PRMT, bool CLC, bool DB = false,
+          int MAXB = NF4_MAX_BATCH>
+__global__ void __launch_bounds__(kThreads) dequant_kernel(const __grid_constant__ BatchParamsT<MAXB> P) {
   constexpr int GROUP = 2 * VEC;                      // elements per thread-group
   constexpr int64_t TILE = int64_t(kThreads) * GROUP * U;
   constexpr int NBUF = DB ? 2 : 1;                    // scale cache / CLC response slots
@@ -394,6 +400,22 @@ static int current_variant() {
 
 static int64_t tile_elems(int v) { return int64_t(kThreads) * 2 * kVariants[v].vec * kVariants[v].unroll; }
 
+template <int MAXB>
+static void launch_small(const BatchParams& P, int out, int grid, cudaStream_t stream) {
+  BatchParamsT<MAXB> Q;
+  Q.total_tiles = P.total_tiles;
+  Q.count = P.count;
+  Q.pad_ = 0;
+  for (int i = 0; i < 16; ++i) Q.lut[i] = P.lut[i];
+  for (int i = 0; i < P.count; ++i) Q.t[i] = P.t[i];
+  if (out == 0)
+    dequant_kernel<0, 8, 4, false, true, true, true, false, MAXB><<<grid, kThreads, 0, stream>>>(Q);
+  else if (out == 1)
+    dequant_kernel<1, 8, 4, false, true, true, true, false, MAXB><<<grid, kThreads, 0, stream>>>(Q);
+  else
+    dequant_kernel<2, 8, 4, false, true, true, true, false, MAXB><<<grid, kThreads, 0, stream>>>(Q);
+}
+
 static KernelFn kernel_of(int out, int v) {
   return out == 0 ? kernel_for<0>(v) : out == 1 ? kernel_for<1>(v) : kernel_for<2>(v);
 }
@@ -471,8 +493,14 @@ static nf4_status launch_batch(const nf4_tensor* ts, int count, int out, const f
   if (P.count == 0) return NF4_OK;
   P.total_tiles = tiles;
   const int grid = grid_for(v, tiles, out);
-  KernelFn fn = kernel_of(out, v);
-  fn<<<grid, kThreads, 0, stream>>>(P);
+  if (v == kDefaultVariant && P.count <= 16) {
+    // light parameter block for single tensors and decoder-layer batches
+    if (P.count == 1) launch_small<1>(P, out, grid, stream);
+    else launch_small<16>(P, out, grid, stream);
+  } else {
+    KernelFn fn = kernel_of(out, v);
+    fn<<<grid, kThreads, 0, stream>>>(P);
+  }
   const cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) {
     cudaGetLastError();

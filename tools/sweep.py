@@ -73,7 +73,7 @@ def main():
                 times = []
                 for _ in range(args.reps):
                     if cold:
-                        torch.sum(flush, dtype=torch.int64, out=sink)
+                        sink.copy_(flush.sum(dtype=torch.int64))
                     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     s.record()
                     f()
