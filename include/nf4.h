@@ -119,7 +119,7 @@ nf4_status nf4_dequantize_batched(const nf4_tensor* tensors, int32_t count, nf4_
 /*
  * nf4_dequantize_host -- the same operation on HOST buffers (end-to-end path:
  * pinned host -> HBM -> kernel -> HBM -> pinned host).  The inputs are copied
- * in chunks of whole second-level groups, dequantized and copied back, double
+ * in chunks of whole second-level groups, dequantized and copied back, triple
  * buffered on `stream` and an internal event chain so copies overlap compute.
  *   packed, absmax, out and the dq arrays (qabsmax, absmax2, code2) are [host]
  *   pointers (pinned memory gives full PCIe/C2C bandwidth; pageable works).
@@ -132,6 +132,18 @@ nf4_status nf4_dequantize_host(const uint8_t* packed, const float* absmax, const
                                void* workspace, int64_t workspace_bytes, int64_t chunk_elems,
                                void* stream);
 int64_t nf4_host_workspace_bytes(int64_t chunk_elems, int32_t blocksize, int32_t dq);
+
+/*
+ * nf4_dequantize_host_batched -- nf4_dequantize_host over `count` tensors whose
+ * chunks form ONE pipeline (no drain/refill between tensors).  Every pointer
+ * in the descriptors (packed, absmax, dq.*, out) is a [host] pointer.  The
+ * workspace must hold nf4_host_workspace_bytes(chunk_elems, smallest blocksize,
+ * any tensor double-quantized); chunk_elems must be a multiple of 256 x the
+ * largest blocksize.  Synchronous like nf4_dequantize_host.
+ */
+nf4_status nf4_dequantize_host_batched(const nf4_tensor* tensors, int32_t count, nf4_dtype out_dtype,
+                                       void* workspace, int64_t workspace_bytes, int64_t chunk_elems,
+                                       void* stream);
 
 /*
  * nf4_quantize -- blockwise NF4 quantization, used to GENERATE inputs

@@ -26,7 +26,7 @@ __all__ = [
     "nf4_synth_fill", "nf4_sol_stream", "nf4_set_max_ctas", "nf4_dequant_grid", "nf4_dequant_tile_elems",
     "nf4_kernel_variants", "nf4_set_kernel_variant", "nf4_get_kernel_variant",
     "nf4_dequantize_ex", "nf4_dequantize_batched_ex", "nf4_codebook_fp4",
-    "nf4_gemm", "nf4_gemm_default_splits", "nf4_gemm_workspace_bytes",
+    "nf4_gemm", "nf4_gemm_default_splits", "nf4_gemm_workspace_bytes", "nf4_dequantize_host_batched",
 ]
 
 
@@ -177,6 +177,17 @@ def nf4_dequantize_host(packed, absmax=None, dq: Optional[DQ] = None, *, n: int,
                                     int(n), int(blocksize), _dtype_code(out_dtype), _ptr(out), _ptr(workspace),
                                     int(nbytes), int(chunk_elems), _stream(stream))
     _lib.check(st, "nf4_dequantize_host")
+
+
+def nf4_dequantize_host_batched(tensors: Sequence[NF4Tensor], out_dtype="f16", *, workspace, chunk_elems: int,
+                                stream=None) -> None:
+    """Host-buffer path over several tensors in one pipeline (all descriptor
+    pointers are host memory; `workspace` is a device buffer)."""
+    arr = (_lib.TensorDesc * max(len(tensors), 1))(*[t.c() for t in tensors])
+    nbytes = workspace.numel() * workspace.element_size()
+    st = load().nf4_dequantize_host_batched(arr, len(tensors), _dtype_code(out_dtype), _ptr(workspace), int(nbytes),
+                                            int(chunk_elems), _stream(stream))
+    _lib.check(st, "nf4_dequantize_host_batched")
 
 
 def nf4_quantize(x, blocksize: int = 64, packed=None, absmax=None, stream=None):

@@ -25,7 +25,7 @@ EXPORTS = [
     "nf4_synth_fill", "nf4_sol_stream", "nf4_set_max_ctas", "nf4_dequant_grid", "nf4_dequant_tile_elems",
     "nf4_kernel_variant_count", "nf4_kernel_variant_name", "nf4_set_kernel_variant", "nf4_get_kernel_variant",
     "nf4_dequantize_ex", "nf4_dequantize_batched_ex", "nf4_codebook_fp4",
-    "nf4_gemm", "nf4_gemm_default_splits", "nf4_gemm_workspace_bytes",
+    "nf4_gemm", "nf4_gemm_default_splits", "nf4_gemm_workspace_bytes", "nf4_dequantize_host_batched",
 ]
 
 
@@ -68,6 +68,7 @@ def load() -> ctypes.CDLL:
             "nf4_dequantize_batched": ([ctypes.POINTER(TensorDesc), i32, i32, P], st),
             "nf4_dequantize_host": ([P, P, ctypes.POINTER(DQState), i64, i32, i32, P, P, i64, i64, P], st),
             "nf4_host_workspace_bytes": ([i64, i32, i32], i64),
+            "nf4_dequantize_host_batched": ([ctypes.POINTER(TensorDesc), i32, i32, P, i64, i64, P], st),
             "nf4_quantize": ([P, i32, i64, i32, P, P, P], st),
             "nf4_double_quantize": ([P, i64, f32, P, i32, P, P, P], st),
             "nf4_codebook": ([P], None),

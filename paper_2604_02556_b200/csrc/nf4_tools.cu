@@ -128,11 +128,15 @@ extern "C" nf4_status nf4_sol_stream(const void* src, int64_t in_bytes, void* ds
 }
 
 // ---------------------------------------------------------------------------
-// Host-buffer pipeline (nf4_dequantize_host)
+// Host-buffer pipeline (nf4_dequantize_host, nf4_dequantize_host_batched)
+// The chunks of all tensors form one stream; kNumSlots workspace slots rotate
+// so that the H2D copy of chunk c+2, the kernel of chunk c+1 and the D2H copy of
+// chunk c overlap (copy engines in both directions + SMs busy at once).
 // ---------------------------------------------------------------------------
 namespace {
+constexpr int kNumSlots = 3;
 struct HostLayout {
-  int64_t codes, scales, groups, out, slot;  // byte sizes (256-B rounded)
+  int64_t codes, scales, groups, code2, out, slot;  // byte sizes (256-B rounded)
 };
 inline int64_t rnd(int64_t v) { return (v + 255) / 256 * 256; }
 HostLayout host_layout(int64_t chunk, int32_t bs, bool dq) {
@@ -141,8 +145,9 @@ HostLayout host_layout(int64_t chunk, int32_t bs, bool dq) {
   L.codes = rnd(chunk / 2);
   L.scales = rnd(dq ? nb : nb * 4);
   L.groups = dq ? rnd((nb / 256) * 4) : 0;
+  L.code2 = dq ? 1024 : 0;
   L.out = rnd(chunk * 2);
-  L.slot = L.codes + L.scales + L.groups + L.out;
+  L.slot = L.codes + L.scales + L.groups + L.code2 + L.out;
   return L;
 }
 }  // namespace
@@ -150,34 +155,46 @@ HostLayout host_layout(int64_t chunk, int32_t bs, bool dq) {
 extern "C" int64_t nf4_host_workspace_bytes(int64_t chunk_elems, int32_t blocksize, int32_t dq) {
   if (chunk_elems <= 0 || !is_pow2(blocksize)) return 0;
   const HostLayout L = host_layout(chunk_elems, blocksize, dq != 0);
-  return 2 * L.slot + (dq ? 1024 : 0);
+  return kNumSlots * L.slot;
 }
 
-extern "C" nf4_status nf4_dequantize_host(const uint8_t* packed, const float* absmax, const nf4_dq_state* dq,
-                                          int64_t n, int32_t blocksize, nf4_dtype out_dtype, void* out,
-                                          void* workspace, int64_t workspace_bytes, int64_t chunk_elems,
-                                          void* stream) {
-  if (n < 0) return NF4_ERR_BAD_SIZE;
-  if (!is_pow2(blocksize) || blocksize < 64 || blocksize > 4096) return NF4_ERR_BAD_BLOCKSIZE;
+extern "C" nf4_status nf4_dequantize_host_batched(const nf4_tensor* tensors, int32_t count, nf4_dtype out_dtype,
+                                                  void* workspace, int64_t workspace_bytes, int64_t chunk_elems,
+                                                  void* stream) {
+  if (count < 0) return NF4_ERR_BAD_SIZE;
+  if (count > 0 && !tensors) return NF4_ERR_NULL_POINTER;
   if (out_dtype != NF4_F16 && out_dtype != NF4_BF16) return NF4_ERR_BAD_DTYPE;
-  if ((absmax == nullptr) == (dq == nullptr)) return NF4_ERR_BAD_STATE;
-  if (dq && dq->blocksize2 != 256) return NF4_ERR_BAD_STATE;
-  if (n == 0) { set_launch_count(0); return NF4_OK; }
-  if (!packed || !out || !workspace) return NF4_ERR_NULL_POINTER;
-  if (dq && (!dq->qabsmax || !dq->code2 || !dq->absmax2)) return NF4_ERR_NULL_POINTER;
-  if (chunk_elems <= 0 || chunk_elems % (int64_t(256) * blocksize) != 0) return NF4_ERR_BAD_SIZE;
+  int32_t bs_min = 4096, bs_max = 64;
+  bool any_dq = false, any_work = false;
+  for (int i = 0; i < count; ++i) {
+    const nf4_tensor& t = tensors[i];
+    if (t.n < 0) return NF4_ERR_BAD_SIZE;
+    if (t.reserved != 0) return NF4_ERR_BAD_STATE;
+    if (!is_pow2(t.blocksize) || t.blocksize < 64 || t.blocksize > 4096) return NF4_ERR_BAD_BLOCKSIZE;
+    const bool dq = t.absmax == nullptr;
+    if (dq && t.dq.blocksize2 != 256) return NF4_ERR_BAD_STATE;
+    if (t.n == 0) continue;
+    if (!t.packed || !t.out) return NF4_ERR_NULL_POINTER;
+    if (dq && (!t.dq.qabsmax || !t.dq.code2 || !t.dq.absmax2)) return NF4_ERR_NULL_POINTER;
+    any_work = true;
+    any_dq = any_dq || dq;
+    bs_min = t.blocksize < bs_min ? t.blocksize : bs_min;
+    bs_max = t.blocksize > bs_max ? t.blocksize : bs_max;
+  }
+  if (!any_work) { set_launch_count(0); return NF4_OK; }
+  if (!workspace) return NF4_ERR_NULL_POINTER;
+  if (chunk_elems <= 0 || chunk_elems % (int64_t(256) * bs_max) != 0) return NF4_ERR_BAD_SIZE;
   if (!aligned(workspace, 256)) return NF4_ERR_MISALIGNED;
-  const bool isdq = dq != nullptr;
-  if (workspace_bytes < nf4_host_workspace_bytes(chunk_elems, blocksize, isdq)) return NF4_ERR_BAD_STATE;
+  if (workspace_bytes < nf4_host_workspace_bytes(chunk_elems, bs_min, any_dq)) return NF4_ERR_BAD_STATE;
 
-  const HostLayout L = host_layout(chunk_elems, blocksize, isdq);
+  const HostLayout L = host_layout(chunk_elems, bs_min, any_dq);
   uint8_t* ws = static_cast<uint8_t*>(workspace);
-  float* d_code2 = isdq ? reinterpret_cast<float*>(ws + 2 * L.slot) : nullptr;
   cudaStream_t cs = (cudaStream_t)stream;
   cudaStream_t h2d = nullptr, d2h = nullptr;
-  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
+  cudaEvent_t ev_in[kNumSlots] = {}, ev_comp[kNumSlots] = {}, ev_out[kNumSlots] = {};
   nf4_status st = NF4_OK;
   int32_t launches = 0;
+  int64_t c = 0;  // global chunk counter
 #define NF4_TRY(x)                       \
   do {                                   \
     if ((x) != cudaSuccess) {            \
@@ -187,58 +204,61 @@ extern "C" nf4_status nf4_dequantize_host(const uint8_t* packed, const float* ab
   } while (0)
   NF4_TRY(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
   NF4_TRY(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < kNumSlots; ++i) {
     NF4_TRY(cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming));
     NF4_TRY(cudaEventCreateWithFlags(&ev_comp[i], cudaEventDisableTiming));
     NF4_TRY(cudaEventCreateWithFlags(&ev_out[i], cudaEventDisableTiming));
   }
-  // h2d must start after everything already queued on the caller's stream
+  // the copies start after everything already queued on the caller's stream
   NF4_TRY(cudaEventRecord(ev_comp[0], cs));
   NF4_TRY(cudaStreamWaitEvent(h2d, ev_comp[0], 0));
-  if (isdq) NF4_TRY(cudaMemcpyAsync(d_code2, dq->code2, 1024, cudaMemcpyHostToDevice, h2d));
-  {
-    const int64_t nchunks = (n + chunk_elems - 1) / chunk_elems;
-    for (int64_t c = 0; c < nchunks; ++c) {
-      const int s = int(c & 1);
+  for (int ti = 0; ti < count; ++ti) {
+    const nf4_tensor& t = tensors[ti];
+    if (t.n == 0) continue;
+    const bool isdq = t.absmax == nullptr;
+    const int32_t bs = t.blocksize;
+    for (int64_t e0 = 0; e0 < t.n; e0 += chunk_elems, ++c) {
+      const int s = int(c % kNumSlots);
       uint8_t* base = ws + s * L.slot;
       uint8_t* d_codes = base;
       uint8_t* d_scales = base + L.codes;
       float* d_groups = reinterpret_cast<float*>(base + L.codes + L.scales);
-      void* d_out = base + L.codes + L.scales + L.groups;
-      const int64_t e0 = c * chunk_elems;
-      const int64_t e1 = (e0 + chunk_elems < n) ? e0 + chunk_elems : n;
+      float* d_code2 = reinterpret_cast<float*>(base + L.codes + L.scales + L.groups);
+      void* d_out = base + L.codes + L.scales + L.groups + L.code2;
+      const int64_t e1 = (e0 + chunk_elems < t.n) ? e0 + chunk_elems : t.n;
       const int64_t m = e1 - e0;
-      const int64_t b0 = e0 / blocksize, b1 = (e1 + blocksize - 1) / blocksize;
-      if (c >= 2) NF4_TRY(cudaStreamWaitEvent(h2d, ev_comp[s], 0));  // inputs of chunk c-2 consumed
-      NF4_TRY(cudaMemcpyAsync(d_codes, packed + e0 / 2, (m + 1) / 2, cudaMemcpyHostToDevice, h2d));
+      const int64_t b0 = e0 / bs, b1 = (e1 + bs - 1) / bs;
+      if (c >= kNumSlots) NF4_TRY(cudaStreamWaitEvent(h2d, ev_comp[s], 0));  // inputs of chunk c-3 consumed
+      NF4_TRY(cudaMemcpyAsync(d_codes, t.packed + e0 / 2, (m + 1) / 2, cudaMemcpyHostToDevice, h2d));
       if (isdq) {
         const int64_t g0 = b0 / 256, g1 = (b1 + 255) / 256;
-        NF4_TRY(cudaMemcpyAsync(d_scales, dq->qabsmax + b0, b1 - b0, cudaMemcpyHostToDevice, h2d));
-        NF4_TRY(cudaMemcpyAsync(d_groups, dq->absmax2 + g0, (g1 - g0) * 4, cudaMemcpyHostToDevice, h2d));
+        NF4_TRY(cudaMemcpyAsync(d_scales, t.dq.qabsmax + b0, b1 - b0, cudaMemcpyHostToDevice, h2d));
+        NF4_TRY(cudaMemcpyAsync(d_groups, t.dq.absmax2 + g0, (g1 - g0) * 4, cudaMemcpyHostToDevice, h2d));
+        NF4_TRY(cudaMemcpyAsync(d_code2, t.dq.code2, 1024, cudaMemcpyHostToDevice, h2d));
       } else {
-        NF4_TRY(cudaMemcpyAsync(d_scales, absmax + b0, (b1 - b0) * 4, cudaMemcpyHostToDevice, h2d));
+        NF4_TRY(cudaMemcpyAsync(d_scales, t.absmax + b0, (b1 - b0) * 4, cudaMemcpyHostToDevice, h2d));
       }
       NF4_TRY(cudaEventRecord(ev_in[s], h2d));
       NF4_TRY(cudaStreamWaitEvent(cs, ev_in[s], 0));
-      if (c >= 2) NF4_TRY(cudaStreamWaitEvent(cs, ev_out[s], 0));  // output slot drained
+      if (c >= kNumSlots) NF4_TRY(cudaStreamWaitEvent(cs, ev_out[s], 0));  // output slot drained
       nf4_status ks;
       if (isdq) {
         nf4_dq_state ld;
         ld.qabsmax = d_scales;
         ld.code2 = d_code2;
         ld.absmax2 = d_groups;
-        ld.offset = dq->offset;
+        ld.offset = t.dq.offset;
         ld.blocksize2 = 256;
-        ks = nf4_dequantize(d_codes, nullptr, &ld, m, blocksize, out_dtype, d_out, cs);
+        ks = nf4_dequantize(d_codes, nullptr, &ld, m, bs, out_dtype, d_out, cs);
       } else {
-        ks = nf4_dequantize(d_codes, reinterpret_cast<const float*>(d_scales), nullptr, m, blocksize, out_dtype,
-                            d_out, cs);
+        ks = nf4_dequantize(d_codes, reinterpret_cast<const float*>(d_scales), nullptr, m, bs, out_dtype, d_out,
+                            cs);
       }
       if (ks != NF4_OK) { st = ks; goto done; }
       launches += nf4_last_launch_count();
       NF4_TRY(cudaEventRecord(ev_comp[s], cs));
       NF4_TRY(cudaStreamWaitEvent(d2h, ev_comp[s], 0));
-      NF4_TRY(cudaMemcpyAsync(static_cast<uint8_t*>(out) + e0 * 2, d_out, m * 2, cudaMemcpyDeviceToHost, d2h));
+      NF4_TRY(cudaMemcpyAsync(static_cast<uint8_t*>(t.out) + e0 * 2, d_out, m * 2, cudaMemcpyDeviceToHost, d2h));
       NF4_TRY(cudaEventRecord(ev_out[s], d2h));
     }
   }
@@ -247,7 +267,7 @@ extern "C" nf4_status nf4_dequantize_host(const uint8_t* packed, const float* ab
   NF4_TRY(cudaStreamSynchronize(cs));
 done:
 #undef NF4_TRY
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < kNumSlots; ++i) {
     if (ev_in[i]) cudaEventDestroy(ev_in[i]);
     if (ev_comp[i]) cudaEventDestroy(ev_comp[i]);
     if (ev_out[i]) cudaEventDestroy(ev_out[i]);
@@ -256,4 +276,31 @@ done:
   if (d2h) { cudaStreamSynchronize(d2h); cudaStreamDestroy(d2h); }
   if (st == NF4_OK) set_launch_count(launches);
   return st;
+}
+
+extern "C" nf4_status nf4_dequantize_host(const uint8_t* packed, const float* absmax, const nf4_dq_state* dq,
+                                          int64_t n, int32_t blocksize, nf4_dtype out_dtype, void* out,
+                                          void* workspace, int64_t workspace_bytes, int64_t chunk_elems,
+                                          void* stream) {
+  if ((absmax == nullptr) == (dq == nullptr)) return NF4_ERR_BAD_STATE;
+  nf4_tensor t;
+  t.packed = packed;
+  t.absmax = absmax;
+  if (dq) {
+    t.dq = *dq;
+  } else {
+    t.dq.qabsmax = nullptr;
+    t.dq.code2 = nullptr;
+    t.dq.absmax2 = nullptr;
+    t.dq.offset = 0.0f;
+    t.dq.blocksize2 = 256;
+  }
+  t.n = n;
+  t.blocksize = blocksize;
+  t.reserved = 0;
+  t.out = out;
+  if (n < 0) return NF4_ERR_BAD_SIZE;
+  if (!is_pow2(blocksize) || blocksize < 64 || blocksize > 4096) return NF4_ERR_BAD_BLOCKSIZE;
+  if (n > 0 && (chunk_elems <= 0 || chunk_elems % (int64_t(256) * blocksize) != 0)) return NF4_ERR_BAD_SIZE;
+  return nf4_dequantize_host_batched(&t, 1, out_dtype, workspace, workspace_bytes, chunk_elems, stream);
 }

@@ -476,3 +476,27 @@ def test_single_tensor_beyond_2_pow_32_elements(nf4, orc):
         assert np.array_equal(out[k0:k1].cpu().numpy().view(np.uint16), ref), b
     del packed, absmax, out
     torch.cuda.empty_cache()
+
+
+def test_host_buffer_batched_pipeline(nf4, orc):
+    """nf4_dequantize_host_batched: ragged tensors of mixed modes and block sizes
+    streamed through one triple-buffered pipeline == oracle."""
+    import torch
+    chunk = 256 * 4096
+    specs = [(3 * chunk + 12345, 64, True), (777, 128, False), (chunk, 4096, True), (2 * chunk - 64, 256, False)]
+    ws = torch.empty(nf4.nf4_host_workspace_bytes(chunk, 64, True), dtype=torch.uint8, device="cuda")
+    descs, refs = [], []
+    for i, (n, bs, dq) in enumerate(specs):
+        packed, kw = _inputs(n, bs, dq, 900 + i)
+        refs.append(_oracle(orc, packed, kw, n, bs, "f16"))
+        out = torch.zeros(n, dtype=torch.int16).pin_memory()
+        pk = torch.from_numpy(packed).pin_memory()
+        if dq:
+            d = nf4.DQ(torch.from_numpy(kw["qabsmax"]).pin_memory(), torch.from_numpy(kw["code2"]).pin_memory(),
+                       torch.from_numpy(kw["absmax2"]).pin_memory(), kw["offset"])
+            descs.append(nf4.NF4Tensor(pk, n, bs, out, None, d))
+        else:
+            descs.append(nf4.NF4Tensor(pk, n, bs, out, torch.from_numpy(kw["absmax"]).pin_memory(), None))
+    nf4.nf4_dequantize_host_batched(descs, "f16", workspace=ws, chunk_elems=chunk)
+    for d, ref in zip(descs, refs):
+        assert np.array_equal(d.out.numpy().view(np.uint16), ref)
