@@ -19,10 +19,20 @@
  *   absmax / dq  as nf4_dequantize (exactly one given); blocksize in
  *            [64, 4096], K a multiple of 64 and of blocksize.
  *   y        [device] M x N row-major, y_dtype NF4_F16, NF4_BF16 or NF4_F32.
- *   splits   split-K factor (<= 0: nf4_gemm_default_splits).  splits > 1 needs
- *            a workspace of nf4_gemm_workspace_bytes(M, N, K, splits) bytes
- *            [device, 16-byte aligned]; partial sums are reduced in split order
- *            (deterministic for a given splits).
+ *   splits   <= 0: stream-K -- the (tile, 64-element k-chunk) stream is cut
+ *            into one equal contiguous range per SM; a tile cut across
+ *            ranges is summed from fp32 partials, in range order, by the CTA
+ *            holding its last piece (same kernel, no second launch).
+ *            >= 1: classic grid, one CTA per (128-feature tile, token tile,
+ *            split) plus a reduction kernel summing in split order
+ *            (nf4_gemm_default_splits gives a makespan-minimising factor).
+ *   workspace  [device, 16-byte aligned] nf4_gemm_workspace_bytes(M, N, K,
+ *            splits) bytes when that is > 0 (NULL/0 allowed otherwise).  For
+ *            stream-K its head holds per-tile counters: it must be ZERO-FILLED
+ *            before its first use; every call leaves it zeroed again, so one
+ *            buffer serves any sequence of calls on one stream (not two
+ *            concurrent calls).  Results are deterministic for a given
+ *            (splits, GPU).
  * Stream-ordered, asynchronous; status codes as nf4.h.
  */
 #ifndef NF4_GEMM_H_

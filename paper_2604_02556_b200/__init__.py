@@ -13,6 +13,7 @@ kernels.  There is no CPU fallback: without the built library every call raises.
 from __future__ import annotations
 
 import ctypes
+import functools
 from dataclasses import dataclass
 from typing import Optional, Sequence
 
@@ -45,6 +46,9 @@ def _ptr(t) -> Optional[int]:
 def _stream(stream) -> Optional[int]:
     if stream is None:
         import torch
+        raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)   # cheap (no Stream object)
+        if raw is not None:
+            return raw(torch.cuda.current_device()) or None
         return torch.cuda.current_stream().cuda_stream or None
     if isinstance(stream, int):
         return stream or None
@@ -275,6 +279,7 @@ def nf4_gemm_default_splits(M: int, N: int, K: int) -> int:
     return int(load().nf4_gemm_default_splits(int(M), int(N), int(K)))
 
 
+@functools.lru_cache(maxsize=4096)
 def nf4_gemm_workspace_bytes(M: int, N: int, K: int, splits: int) -> int:
     return int(load().nf4_gemm_workspace_bytes(int(M), int(N), int(K), int(splits)))
 
@@ -282,19 +287,20 @@ def nf4_gemm_workspace_bytes(M: int, N: int, K: int, splits: int) -> int:
 def nf4_gemm(x, packed, absmax=None, dq: Optional[DQ] = None, *, N: int, K: int, blocksize: int = 64,
              y=None, y_dtype="bf16", splits: int = 0, workspace=None, stream=None):
     """Y = X . W^T with W the NF4 weight [N, K] dequantized on the fly.
-    x: CUDA tensor [M, K] bf16/fp16.  Allocates y (and the split-K workspace) with
-    torch when not given; returns y."""
+    x: CUDA tensor [M, K] bf16/fp16.  splits <= 0: stream-K over all resident CTAs
+    (default); splits >= 1: classic split-K grid.  Allocates y (and the partial-sum
+    workspace) with torch when not given; returns y."""
     import torch
     M = x.shape[0] if x.dim() == 2 else x.numel() // K
     ycode = _dtype_code(y_dtype)
     if y is None:
         tdt = {_lib.NF4_F16: torch.float16, _lib.NF4_BF16: torch.bfloat16, _lib.NF4_F32: torch.float32}[ycode]
         y = torch.empty((M, N), dtype=tdt, device=x.device)
-    if splits <= 0:
-        splits = nf4_gemm_default_splits(M, N, K)
+    if splits < 0:
+        splits = 0
     wbytes = nf4_gemm_workspace_bytes(M, N, K, splits)
     if wbytes > 0 and workspace is None:
-        workspace = torch.empty(wbytes, dtype=torch.uint8, device=x.device)
+        workspace = torch.zeros(wbytes, dtype=torch.uint8, device=x.device)   # stream-K counters start at 0
     wsize = 0 if workspace is None else workspace.numel() * workspace.element_size()
     dqc = dq.c() if dq is not None else None
     st = load().nf4_gemm(_ptr(x), _dtype_code(x.dtype), int(M), _ptr(packed), _ptr(absmax),

@@ -45,6 +45,26 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(name: str, defines: dict) -> str:
+    """Diagnostics only (tools/): the same sources with extra -D macros, e.g.
+    NF4_GEMM_DIAG=1 (event traces / pipeline-skipping experiments), into
+    <repo>/_variants/libnf4_<name>.so; load it with NF4_LIB=<path>."""
+    out_dir = os.path.join(ROOT, "_variants")
+    os.makedirs(out_dir, exist_ok=True)
+    out = os.path.join(out_dir, f"libnf4_{name}.so")
+    srcs = [os.path.join(CSRC, s) for s in SOURCES] + [os.path.join(CSRC, h) for h in HEADERS]
+    if os.path.exists(out) and all(os.path.getmtime(d) <= os.path.getmtime(out) for d in srcs):
+        return out
+    cmd = [NVCC, *NVCC_FLAGS, *[f"-D{k}={v}" for k, v in defines.items()], "-o", out + ".tmp"] + \
+        [os.path.join(CSRC, s) for s in SOURCES]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc failed building " + out)
+    os.replace(out + ".tmp", out)
+    return out
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)
     print(LIB)

@@ -12,6 +12,12 @@ import threading
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "libnf4.so")
 
+
+def lib_path() -> str:
+    """The in-tree library; NF4_LIB (diagnostics, tools/) may name an alternative
+    build of the same sources, read when the library is first loaded."""
+    return os.path.abspath(os.environ["NF4_LIB"]) if os.environ.get("NF4_LIB") else LIB_PATH
+
 NF4_OK = 0
 NF4_F16, NF4_BF16, NF4_F32 = 0, 1, 2
 NF4_SYNTH_CODES, NF4_SYNTH_ABSMAX, NF4_SYNTH_QABSMAX, NF4_SYNTH_ABSMAX2 = 1, 2, 3, 4
@@ -57,10 +63,11 @@ def load() -> ctypes.CDLL:
     with _lock:
         if _lib is not None:
             return _lib
-        if not os.path.exists(LIB_PATH):
-            raise ImportError(f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+        path = lib_path()
+        if not os.path.exists(path):
+            raise ImportError(f"{path} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
                               "(nvcc, sm_100a).  There is no CPU fallback.")
-        lib = ctypes.CDLL(LIB_PATH)
+        lib = ctypes.CDLL(path)
         P, i64, i32, f32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_float
         st = ctypes.c_int
         sig = {

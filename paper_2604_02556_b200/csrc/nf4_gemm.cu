@@ -12,30 +12,35 @@
 // one it leaves open.
 //
 // Roles (320 threads):
-//   warp 9     TMA issuer (one lane): per 64-element k-chunk, a 2-D TMA box of
-//              the packed codes (128 rows x 32 B) and a 2-D TMA box of X
-//              (BN rows x 64 elements, SWIZZLE_128B: lands directly in the UMMA
-//              canonical layout, zero-filled past M) -> tma_full[s].
-//   warps 0-7  producers: threads 2r, 2r+1 own W row n0+r; each reads its 16
-//              code bytes from shared memory, dequantizes 32 weights into 4 of
-//              the row's 8 swizzled 16-B chunks, fence.proxy.async, arrive
-//              w_full[s].  After the K loop they are the epilogue: warp w reads
-//              TMEM lanes 32(w%4).. and column half w/4 with tcgen05.ld.
-//   warp 8     TMEM allocator and MMA issuer: waits tma_full[s] + w_full[s],
-//              issues 4 x tcgen05.mma (K=16 each), tcgen05.commit -> empty[s];
-//              after the last chunk commits -> done.
-// (A first version had every producer thread load its own row's codes: row-
-// strided 16-B loads cost 32 L1 wavefronts per warp instruction and capped the
-// kernel at ~0.5 TB/s; TMA boxes fetch the same bytes with full-line requests.)
+//   warp 9     TMA issuer (one lane): per super-stage (SUB 64-element chunks)
+//              one 2-D TMA box of packed codes (128 rows x SUB*32 B, swizzled)
+//              and SUB boxes of X (BN rows x 64, SWIZZLE_128B: directly in the
+//              UMMA canonical layout, zero-filled past M).
+//   warps 0-7  producers: thread (w, l) owns weight row 32(w%4)+l (= TMEM lane)
+//              and half w/4 of every chunk; it dequantizes 32 weights and
+//              writes them to TMEM with tcgen05.st -- the A operand of the MMA.
+//              At the end of each segment they are the epilogue (tcgen05.ld).
+//   warp 8     TMEM allocator and MMA issuer: tcgen05.mma.kind::f16 with A in
+//              TMEM and B (X) in shared memory, tcgen05.commit to the barriers.
 // Swap-AB orientation: the MMA's M=128 side is the weight (128 output
 // features), its N side the tokens (BN in {16,...,256}), so decode-size M
-// wastes nothing.  Split-K over gridDim.z writes fp32 partials to a caller
-// workspace; nf4_gemm_reduce sums them in split order (deterministic).
+// wastes nothing.
+// Work distribution (stream-K): the (tile, 64-element k-chunk) stream of the
+// whole GEMM is cut into gridDim.x equal contiguous ranges, one per resident
+// CTA (SMs x CTAs/SM), so every SM gets the same work and no second, partial
+// wave exists; a CTA's range covers 1-3 "segments" (a tile's k-sub-range),
+// each accumulated in TMEM and written as an fp32 partial; nf4_gemm_reduce
+// sums a tile's partials in segment order (deterministic for a given GPU).
+// The classic grid (one CTA per tile x split, explicit `splits`) is the same
+// kernel with one segment per CTA.
 #include <cuda.h>  // CUtensorMap (the encoder is fetched at run time; no libcuda link)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
+#include <type_traits>
 
 #include "nf4_internal.cuh"
 #include "../../include/nf4_gemm.h"
@@ -43,9 +48,7 @@
 namespace nf4 {
 namespace gemm {
 
-constexpr int kProducers = 256;             // 2 threads per weight row (32 elements each)
-constexpr int kProducerWarps = kProducers / 32;
-constexpr int kThreads = kProducers + 64;   // + MMA warp + TMA warp
+constexpr int kProducerWarps = 8;          // per producer group: 2 threads per weight row (32 elements each)
 constexpr int kCodeBytes = 32;              // packed bytes per row per k-chunk
 constexpr int kChunk = 64;          // k elements per stage (= one 128 B swizzle row in 16-bit)
 constexpr int kRowBytes = 128;
@@ -58,13 +61,22 @@ struct GemmParams {
   const float* absmax2;
   const uint16_t* x;       // [M, K] 16-bit
   void* y;                 // [M, N] (splits == 1)
-  float* partial;          // [splits, M, N] fp32 (splits > 1)
+  float* partial;          // [splits, M, N] fp32 (splits > 1) / [parts, M, N] (stream-K)
+  unsigned* flags;         // stream-K: per-tile count of published partials (zero between calls)
   float offset;
   int32_t M, N, K;
   int32_t bs_shift;
-  int32_t chunks_per_split;
-  int32_t splits;
-  int32_t out_dtype;       // NF4_F16 / NF4_BF16 / NF4_F32
+  int32_t chunks_per_split;  // classic split-K
+  int32_t splits;            // classic split-K (1 = direct output)
+  int32_t out_dtype;         // NF4_F16 / NF4_BF16 / NF4_F32
+  int32_t streamk;           // 1: stream-K ranges over a 1-D grid
+  int32_t tiles_n, tiles_m;  // tile grid (128 features x BN tokens)
+  int32_t nk;                // 64-element chunks per tile (K / 64)
+  int64_t total_chunks;      // tiles_n * tiles_m * nk
+  int32_t align4;            // stream-K range bounds rounded to 4 chunks
+  unsigned long long* trace;  // diagnostics only (NF4_GEMM_TRACE): per-CTA start / end / SM / last epilogue
+  int32_t experiment;         // diagnostics only (NF4_GEMM_EXPERIMENT): 1 skip MMA, 2 skip dequant, 4 skip tcgen05.st,
+                              // 8 skip X loads, 16 skip code loads
   float lut[16];
 };
 
@@ -77,15 +89,41 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+#ifndef NF4_GEMM_WAIT_MODE
+#define NF4_GEMM_WAIT_MODE 1
+#endif
+// 0: try_wait with a 10 ms suspend hint; 1: try_wait (hardware default time
+// limit); 2: test_wait spin; >2: try_wait + __nanosleep(mode) between polls.
 __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
   const uint32_t b = smem_u32(bar);
   uint32_t done = 0;
   while (!done) {
+#if NF4_GEMM_WAIT_MODE == 0
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.b32 %0, 1, 0, p;\n\t}"
         : "=r"(done) : "r"(b), "r"(parity), "r"(0x989680) : "memory");
+#elif NF4_GEMM_WAIT_MODE == 1
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, p;\n\t}"
+        : "=r"(done) : "r"(b), "r"(parity) : "memory");
+#elif NF4_GEMM_WAIT_MODE == 2
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, p;\n\t}"
+        : "=r"(done) : "r"(b), "r"(parity) : "memory");
+#else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, p;\n\t}"
+        : "=r"(done) : "r"(b), "r"(parity) : "memory");
+    if (!done) __nanosleep(NF4_GEMM_WAIT_MODE);
+#endif
   }
 }
 
@@ -102,6 +140,75 @@ __device__ __forceinline__ uint32_t umma_idesc(int n, bool bf16) {
   return (1u << 4) | (fmt << 7) | (fmt << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(128 >> 4) << 24);
 }
 
+// Issued by a whole (converged) warp; elect.sync picks the one lane that issues,
+// so every operand is warp-uniform and the four K=16 steps of a 64-element
+// chunk cost ~1 instruction each (a divergent single-lane issue made ptxas
+// rebuild the uniform operands per MMA, ~15 instructions and ~66 cycles each).
+// A: 128 lanes x 16 weights at a, a+8, a+16, a+24 (TMEM columns); B: the
+// SWIZZLE_128B X tile, +32 B (= +2 in the descriptor's address field) per step.
+__device__ __forceinline__ void umma_chunk_elect(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred e, p0, pt;\n\t.reg .b64 b1, b2, b3;\n\t.reg .b32 a1, a2, a3;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p0, %4, 0;\n\tsetp.eq.b32 pt, %4, %4;\n\t"
+      "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+      "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, pt;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], b2, %3, pt;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b3, %3, pt;\n\t}"
+      ::"r"(d), "r"(a), "l"(b), "r"(idesc), "r"(acc) : "memory");
+}
+__device__ __forceinline__ void umma_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}"
+      ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Diagnostics (tools/, a -DNF4_GEMM_DIAG=1 build only; compiled out of libnf4):
+// NF4_GEMM_TRACE = device address of an int64 buffer for event times,
+// NF4_GEMM_EXPERIMENT = bit mask skipping parts of the pipeline (timing studies).
+#ifndef NF4_GEMM_DIAG
+#define NF4_GEMM_DIAG 0
+#endif
+#define NF4_EXP(bit) (NF4_GEMM_DIAG && (p.experiment & (bit)))
+#define NF4_TRACING (NF4_GEMM_DIAG && p.trace != nullptr)
+// per-super-stage event times of CTA 0, slot base + J (J < 80)
+#define NF4_TRACE_J(base, Jv)                                                                       \
+  do {                                                                                              \
+    if (NF4_TRACING && cta_lin == 0 && (Jv) < 80) p.trace[(base) + (Jv)] = gtimer();               \
+  } while (0)
+// ---- stream-K range arithmetic (shared by the GEMM kernel and the reduction) ----
+// First global chunk of CTA c's range: floor(c*W/G), rounded to a multiple of 4
+// chunks when every tile has a multiple of 4 chunks (whole TMA super-stages).
+__host__ __device__ __forceinline__ int64_t sk_bound(int64_t c, int64_t W, int64_t G, int align4) {
+  int64_t b = c * W / G;
+  if (align4) b = (b + 2) / 4 * 4;
+  return b < W ? b : W;
+}
+// The CTA whose range contains global chunk x (largest c with sk_bound(c) <= x):
+// start from floor(x*G/W), whose bound is within 2 chunks of x, and step.
+__host__ __device__ __forceinline__ int64_t sk_owner(int64_t x, int64_t W, int64_t G, int align4) {
+  int64_t c = x * G / W;
+  if (c > G - 1) c = G - 1;
+  while (c > 0 && sk_bound(c, W, G, align4) > x) --c;
+  while (c + 1 < G && sk_bound(c + 1, W, G, align4) <= x) ++c;
+  return c;
+}
+
+// One segment = a contiguous k-range of one output tile processed by one CTA.
+struct Segment {
+  int n0, m0;     // tile origin (features, tokens)
+  int kc0, nk;    // first chunk within the tile, chunk count
+  int part;       // partial-sum slot (stream-K: segment index within the tile; classic: split)
+};
+
 __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
@@ -110,235 +217,464 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* m
       : "memory");
 }
 
-// TMEM column budget: the fp32 accumulator (BN columns) at column 0, then
-// STAGES dequantized A tiles of 32 columns (128 lanes x 64 16-bit weights).
-template <int BN, int STAGES>
-__host__ __device__ constexpr int tmem_cols() {
-  constexpr int need = (BN < 32 ? 32 : BN) + STAGES * 32;
-  return need <= 32 ? 32 : need <= 64 ? 64 : need <= 128 ? 128 : need <= 256 ? 256 : 512;
+// Code-box swizzle: the TMA writes the 128 rows x (SUB*32) B box with the
+// hardware swizzle matching its width, so the 8 lanes of an LDS.128 phase
+// (consecutive rows, same 16-B column) hit 8 different bank groups.
+template <int SUB>
+__device__ __forceinline__ uint32_t code_chunk_off(int row, int c16) {
+  if constexpr (SUB == 4) return uint32_t(row * 128 + ((c16 ^ (row & 7)) << 4));          // SWIZZLE_128B
+  else if constexpr (SUB == 2) return uint32_t(row * 64 + ((c16 ^ ((row >> 1) & 3)) << 4));  // SWIZZLE_64B
+  else return uint32_t(row * 32 + ((c16 ^ ((row >> 2) & 1)) << 4));                          // SWIZZLE_32B
 }
 
-template <int BN, int STAGES, int RING, bool BF16>
-__global__ void __launch_bounds__(kThreads, 1)
+// Segment enumeration: every role walks the same sequence.  Stream-K ranges are
+// computed once per CTA by one thread; only a range's first segment can start
+// inside a tile, so every later segment is its tile's partial slot 0.
+struct SegIter {
+  int x, end, start;   // stream-K: global chunk cursor, range end, range start
+  int part0;           // slot of the first segment
+  int done_classic;
+};
+template <int BN>
+__device__ __forceinline__ bool next_segment(const GemmParams& p, SegIter& it, Segment& sg) {
+  if (!p.streamk) {
+    if (it.done_classic) return false;
+    it.done_classic = 1;
+    sg.n0 = blockIdx.x * 128;
+    sg.m0 = blockIdx.y * BN;
+    sg.kc0 = blockIdx.z * p.chunks_per_split;
+    const int kc1 = min(p.nk, sg.kc0 + p.chunks_per_split);
+    sg.nk = kc1 > sg.kc0 ? kc1 - sg.kc0 : 0;
+    sg.part = blockIdx.z;
+    return true;
+  }
+  if (it.x >= it.end) return false;
+  const int tile = it.x / p.nk;
+  const int tstart = tile * p.nk;
+  const int send = min(it.end, tstart + p.nk);
+  sg.n0 = (tile % p.tiles_n) * 128;
+  sg.m0 = (tile / p.tiles_n) * BN;
+  sg.kc0 = it.x - tstart;
+  sg.nk = send - it.x;
+  sg.part = it.x == it.start ? it.part0 : 0;
+  it.x = send;
+  return true;
+}
+__device__ __forceinline__ SegIter seg_begin(const int (&range)[3]) {
+  SegIter it;
+  it.done_classic = 0;
+  it.start = it.x = range[0];
+  it.end = range[1];
+  it.part0 = range[2];
+  return it;
+}
+
+// Block scales of one super-stage for one weight row.  fast: blocksize 64,
+// K % 256 == 0, 4-chunk super-stages -- the 4 scales are 4 consecutive fp32
+// absmax (one 128-bit load) or 4 consecutive qabsmax bytes (one 32-bit load)
+// plus the 1-2 absmax2 groups they fall in; general: one load per chunk.
+struct Scales {
+  uint32_t s[4];   // fp32 absmax bits per chunk | fast DQ: 4 qabsmax bytes in s[0] | DQ: qabsmax per chunk
+  float a2[4];     // DQ: absmax2 per chunk | fast DQ: absmax2 of the first / last block in a2[0] / a2[1]
+};
+
+// One CTA per SM, G groups of 8 producer warps sharing one TMA/MMA pipeline
+// (a single CTA keeps the SM's work in one stream-K range: with 3 independent
+// CTAs per SM the warp scheduler starved the youngest, whose tail then ran
+// alone -- tools/gemm_trace.py measured 21-43 us for equal ranges).
+//   warps 0..8G-1  producers; group g = warp/8 dequantizes the super-stages J
+//                  with J % G == g, thread (w, l) owning weight row
+//                  32(w%4)+l (= TMEM lane) and half (w%8)/4 of each chunk;
+//                  the group that produced a segment's last super-stage then
+//                  runs its epilogue (tcgen05.ld -> y or fp32 partial).
+//   warp 8G        TMEM allocator + MMA issuer (one lane).
+//   warp 8G+1      TMA issuer (one lane).
+// TMEM: NACC accumulators of max(BN, 32) fp32 columns, then G*SUB A tiles of
+// 32 columns (128 lanes x 64 16-bit weights), one per (group, chunk-in-stage).
+// Barriers (one arrive/commit per super-stage each, so the single MMA thread
+// spends its time issuing MMAs, not waiting on barriers): c_full (TMA bytes) /
+// c_free (MMA commit: the MMA waited for w_full, so the codes were read too)
+// per shared-memory super-stage (CST >= G keeps every parity wait within one
+// phase); w_full (8 warps) / a_free (MMA commit) per group's 4 A tiles;
+// acc_full / acc_empty per accumulator.
+// Stream-K fix-up (no second kernel): every tile piece that is not the tile's
+// last is published as an fp32 partial + a per-tile counter increment; the CTA
+// holding the tile's last piece (its range's first segment) sums the partials
+// in piece order at the end of its range and writes y.  It waits only for
+// lower-numbered CTAs, dispatched before it.
+template <int BN, int G, int SUB, int CST, int NACC, bool BF16>
+__global__ void __launch_bounds__(32 * (8 * G + 2), 1)
     nf4_gemm_kernel(const __grid_constant__ GemmParams p, const __grid_constant__ CUtensorMap map_codes,
                     const __grid_constant__ CUtensorMap map_x) {
+  static_assert(CST >= G, "a super-stage slot must not be two phases behind any group");
+  constexpr int kMmaWarp = 8 * G, kTmaWarp = 8 * G + 1;
+  constexpr int ACC = BN < 32 ? 32 : BN;
+  constexpr int A0 = NACC * ACC;
+  static_assert(A0 + G * SUB * 32 <= 512, "TMEM budget");
+  constexpr int kSuperCodeBytes = 128 * SUB * kCodeBytes;
+  constexpr int kSuperXBytes = SUB * BN * kRowBytes;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // 1024-B alignment for the swizzle atoms (offset arithmetic on the __shared__
-  // array keeps the shared address space visible to the compiler: LDS/STS)
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* smem_x = smem;                                     // STAGES x BN x 128 B (X, SW128, by TMA)
-  uint8_t* smem_c = smem_x + STAGES * BN * kRowBytes;         // STAGES x 4 KB (packed codes, by TMA)
-  uint64_t* tma_full = reinterpret_cast<uint64_t*>(smem_c + STAGES * 128 * kCodeBytes);
-  uint64_t* w_full = tma_full + STAGES;
-  uint64_t* empty = w_full + STAGES;
-  uint64_t* done = empty + STAGES;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(done + 1);
   __shared__ __align__(256) float lut[16];                    // 256-B aligned: address = PRMT(offsets, base)
   __shared__ float code2s[256];                               // DQ second-level table
+  __shared__ __align__(8) uint64_t c_full[CST], c_free[CST], w_full[G], a_free[G], acc_full[NACC], acc_empty[NACC];
+  __shared__ uint32_t tmem_holder;
+  __shared__ int sk_range[3];                                 // stream-K: range start, end, first slot
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* smem_c = smem;                                     // CST x 128 rows x SUB*32 B (codes)
+  uint8_t* smem_x = smem_c + CST * kSuperCodeBytes;           // CST x SUB x BN x 128 B (X)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * 128;
-  const int m0 = blockIdx.y * BN;
-  const int split = blockIdx.z;
-  const int nk_total = p.K / kChunk;
-  const int kc0 = split * p.chunks_per_split;
-  const int kc1 = min(nk_total, kc0 + p.chunks_per_split);
-  const int nk = kc1 > kc0 ? kc1 - kc0 : 0;
-  constexpr int TMEM_COLS = tmem_cols<BN, STAGES>();
-  constexpr int ACC_COLS = BN < 32 ? 32 : BN;                 // A stages start here (32-column aligned)
-  constexpr uint32_t kStageTx = 128 * kCodeBytes + BN * kRowBytes;
-
+  const int cta_lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  if (NF4_TRACING && threadIdx.x == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    p.trace[1024 + 4 * cta_lin] = gtimer();
+    p.trace[1024 + 4 * cta_lin + 2] = smid;
+  }
   if (threadIdx.x < 16) lut[threadIdx.x] = p.lut[threadIdx.x];
   if (p.absmax == nullptr) {
-    for (int i = threadIdx.x; i < 256; i += kThreads) code2s[i] = p.code2[i];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) code2s[i] = p.code2[i];
   }
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&tma_full[s], 1);
-      mbar_init(&w_full[s], kProducerWarps);   // one elected arrive per producer warp
-      mbar_init(&empty[s], 1);
+    for (int s = 0; s < CST; ++s) {
+      mbar_init(&c_full[s], 1);
+      mbar_init(&c_free[s], 1);
     }
-    mbar_init(done, 1);
+    for (int s = 0; s < G; ++s) {
+      mbar_init(&w_full[s], kProducerWarps);
+      mbar_init(&a_free[s], 1);
+    }
+    for (int s = 0; s < NACC; ++s) {
+      mbar_init(&acc_full[s], 1);
+      mbar_init(&acc_empty[s], kProducerWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (p.streamk) {
+      const int64_t W = p.total_chunks, NG = gridDim.x;
+      const int64_t x0 = sk_bound(blockIdx.x, W, NG, p.align4);
+      sk_range[0] = int(x0);
+      sk_range[1] = int(sk_bound(blockIdx.x + 1, W, NG, p.align4));
+      sk_range[2] = int(blockIdx.x - sk_owner(x0 / p.nk * p.nk, W, NG, p.align4));
+    } else {
+      sk_range[0] = sk_range[1] = sk_range[2] = 0;
+    }
   }
-  if (warp == kProducerWarps) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
-                 "n"(TMEM_COLS) : "memory");
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_holder))
+                 : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
-  if (warp == kProducerWarps + 1 && lane == 0) {
+  if (warp == kTmaWarp && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_codes)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_x)) : "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem = *tmem_holder;
+  const uint32_t tmem = tmem_holder;
+  if (NF4_TRACING && cta_lin == 0 && threadIdx.x == 0) p.trace[0] = gtimer();
 
-  if (warp < kProducerWarps) {
-    // ======================= producers (dequantize into TMEM) =======================
-    // Warp w may only address TMEM lanes 32(w%4)..32(w%4)+31, so thread (w, l)
-    // owns weight row r = 32(w%4)+l of the tile and k-half h = w/4 (32 of the
-    // chunk's 64 elements).  The block-scale inputs of chunk i+RING are loaded
-    // while chunk i is dequantized (register ring); the codes arrive by TMA.
-    const int t = 32 * (warp & 3) + lane;      // tile row = TMEM lane
-    const int half = warp >> 2;
-    const int row = n0 + t;                    // weight row (output feature)
-    const bool row_ok = row < p.N;
-    const int64_t blk_base = (int64_t(row) * p.K) >> p.bs_shift;
+  if (warp < 8 * G) {
+    // ======================= producers (dequantize into TMEM) + epilogue =======================
+    const int g = warp >> 3, wl = warp & 7;
+    const int t = 32 * (wl & 3) + lane;        // tile row = TMEM lane
+    const int half = wl >> 2;
     const int chunk_shift = p.bs_shift - 6;    // 64-element chunks per quantization block = 2^chunk_shift
-    const uint32_t tlane = uint32_t(32 * (warp & 3)) << 16;
+    const uint32_t tlane = uint32_t(32 * (wl & 3)) << 16;
     const uint32_t lut_base = smem_u32(lut);   // low byte 0: PRMT splices a byte offset into it
-    uint32_t rq[RING];     // fp32 absmax bits, or qabsmax (DQ)
-    float ra2[RING];       // absmax2 (DQ)
-    auto issue = [&](int d, int i) {
-      rq[d] = 0;
-      ra2[d] = 0.0f;
-      if (row_ok) {
-        const int64_t b = blk_base + ((kc0 + i) >> chunk_shift);
-        if (p.absmax != nullptr) {
-          rq[d] = __float_as_uint(__ldg(p.absmax + b));
-        } else {
-          rq[d] = __ldg(p.qabsmax + b);
-          ra2[d] = __ldg(p.absmax2 + (b >> 8));
-        }
-      }
-    };
+    int J = 0, sidx = 0;                       // super-stages / segments before this segment
+    SegIter it = seg_begin(sk_range);
+    Segment sg;
+    while (next_segment<BN>(p, it, sg)) {
+      const int row = sg.n0 + t;
+      const bool row_ok = row < p.N;
+      const int64_t blk_base = (int64_t(row) * p.K) >> p.bs_shift;
+      const int nk = sg.nk, kc0 = sg.kc0;
+      const int nsuper = (nk + SUB - 1) / SUB;
+      const bool fast =
+          SUB == 4 && p.bs_shift == 6 && (p.K % 256) == 0 && (kc0 % 4) == 0 &&
+          (p.absmax != nullptr ? (reinterpret_cast<uintptr_t>(p.absmax) & 15) == 0
+                               : (reinterpret_cast<uintptr_t>(p.qabsmax) & 3) == 0);
+      auto fetch = [&](Scales& sc, int j) {
 #pragma unroll
-    for (int d = 0; d < RING; ++d)
-      if (d < nk) issue(d, d);
-    for (int i0 = 0; i0 < nk; i0 += RING) {
-#pragma unroll
-      for (int d = 0; d < RING; ++d) {
-        const int i = i0 + d;
-        if (i >= nk) break;
-        const int s = i % STAGES;
-        // block scale (A4): fp32 absmax, or fl32(fl32(code2[q] * absmax2) + offset)
-        const float a = p.absmax != nullptr ? __uint_as_float(rq[d])
-                                            : __fadd_rn(__fmul_rn(code2s[rq[d]], ra2[d]), p.offset);
-        if (i + RING < nk) issue(d, i + RING);
-        mbar_wait_parity(&tma_full[s], (i / STAGES) & 1);   // codes (and X) landed; A stage s is free
-        const uint4 c0 = *reinterpret_cast<const uint4*>(smem_c + s * 128 * kCodeBytes + t * kCodeBytes + 16 * half);
-        // dequantize 32 weights: word j = (element 2j) | (element 2j+1) << 16
-        const uint32_t cw[4] = {c0.x, c0.y, c0.z, c0.w};
-        const uint64_t aa = f32x2_splat(a);
-        uint32_t w[16];
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          const uint32_t x = cw[cc];
-          const uint32_t hi4 = (x >> 2) & 0x3C3C3C3Cu;  // byte j = 4 * high nibble (LUT byte offset)
-          const uint32_t lo4 = (x << 2) & 0x3C3C3C3Cu;  // byte j = 4 * low nibble
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            // shared address of NF4[idx] = lut_base with byte 0 replaced by byte j of hi4/lo4: one PRMT
-            const uint32_t ah = __byte_perm(hi4, lut_base, 0x7650u + j);
-            const uint32_t al = __byte_perm(lo4, lut_base, 0x7650u + j);
-            float ch, cl;
-            asm("ld.shared.f32 %0, [%1];" : "=f"(ch) : "r"(ah));
-            asm("ld.shared.f32 %0, [%1];" : "=f"(cl) : "r"(al));
-            mul2_rn(ch, cl, aa);                      // fl32(NF4[idx] * a) for both, one FMUL2
-            w[4 * cc + j] = pack2_rn<BF16>(ch, cl);
+        for (int q = 0; q < 4; ++q) { sc.s[q] = 0; sc.a2[q] = 0.0f; }
+        if (!row_ok) return;
+        if (fast) {
+          const int64_t b0 = blk_base + kc0 + 4 * j;
+          if (p.absmax != nullptr) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(p.absmax + b0));
+            sc.s[0] = v.x; sc.s[1] = v.y; sc.s[2] = v.z; sc.s[3] = v.w;
+          } else {
+            sc.s[0] = __ldg(reinterpret_cast<const uint32_t*>(p.qabsmax + b0));
+            sc.a2[0] = __ldg(p.absmax2 + (b0 >> 8));
+            sc.a2[1] = __ldg(p.absmax2 + ((b0 + 3) >> 8));
           }
-        }
-        // 16 columns (32 weights) of this row's A tile in TMEM
-        const uint32_t taddr = tmem + tlane + uint32_t(ACC_COLS + s * 32 + half * 16);
-        asm volatile(
-            "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
-            ::"r"(taddr), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]),
-            "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]), "r"(w[15])
-            : "memory");
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&w_full[s]);
-      }
-    }
-    // ======================= epilogue =======================
-    mbar_wait_parity(done, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int q = warp & 3;                          // TMEM lane quarter this warp may access
-    constexpr int HB = BN / 2 < 16 ? 16 : BN / 2;    // columns per warp (BN = 16: warps 4-7 idle)
-    const int col0 = (warp >> 2) * HB;
-    const int n = n0 + q * 32 + lane;
-    const uint32_t taddr = tmem + (uint32_t(q * 32) << 16);
+        } else {
 #pragma unroll
-    for (int cb = col0; cb < col0 + HB && cb < BN; cb += 16) {
-      uint32_t v[16];
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-          : "r"(taddr + cb));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (n < p.N) {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int m = m0 + cb + j;
-          if (m < p.M) {
-            const float acc = nk > 0 ? __uint_as_float(v[j]) : 0.0f;
-            if (p.splits > 1) {
-              p.partial[(int64_t(split) * p.M + m) * p.N + n] = acc;
-            } else if (p.out_dtype == NF4_F32) {
-              static_cast<float*>(p.y)[int64_t(m) * p.N + n] = acc;
-            } else {
-              static_cast<uint16_t*>(p.y)[int64_t(m) * p.N + n] =
-                  p.out_dtype == NF4_BF16 ? cvt1_rn<true>(acc) : cvt1_rn<false>(acc);
+          for (int q = 0; q < SUB; ++q) {
+            const int i = j * SUB + q;
+            if (i < nk) {
+              const int64_t b = blk_base + ((kc0 + i) >> chunk_shift);
+              if (p.absmax != nullptr) {
+                sc.s[q] = __float_as_uint(__ldg(p.absmax + b));
+              } else {
+                sc.s[q] = __ldg(p.qabsmax + b);
+                sc.a2[q] = __ldg(p.absmax2 + (b >> 8));
+              }
             }
           }
         }
+      };
+      int j = (g - J % G + G) % G;               // this group's first super-stage of the segment
+      Scales nxt;
+      if (j < nsuper) fetch(nxt, j);
+      for (; j < nsuper; j += G) {
+        const Scales sc = nxt;
+        if (j + G < nsuper) fetch(nxt, j + G);   // one super-stage ahead (hides the L2 latency)
+        const int Jg = J + j;
+        const int cs = Jg % CST;
+        const uint32_t aph = uint32_t(Jg / G) & 1u;
+        mbar_wait_parity(&c_full[cs], uint32_t(Jg / CST) & 1u);   // codes + X of this super-stage landed
+        if (wl == 0 && lane == 0) NF4_TRACE_J(100, Jg);
+        mbar_wait_parity(&a_free[g], aph ^ 1u);                    // the MMA is done with our previous A tiles
+        if (wl == 0 && lane == 0) NF4_TRACE_J(200, Jg);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int64_t b0 = blk_base + kc0 + 4 * j;
+        // the stage body, specialised on "all SUB chunks present" and the scale format
+        // (uniform branches hoisted out of the per-chunk code)
+        auto stage = [&](auto full_tag, auto mode_tag) {
+          constexpr bool FULL = decltype(full_tag)::value;
+          constexpr int MODE = decltype(mode_tag)::value;   // 0 fp32 absmax, 1 DQ fast, 2 DQ general
+#pragma unroll
+          for (int q = 0; q < SUB; ++q) {
+            const int i = j * SUB + q;
+            if (!FULL && i >= nk) break;
+            uint32_t w[16];
+            if (!NF4_EXP(2)) {
+              float a;
+              if constexpr (MODE == 0) {
+                a = __uint_as_float(sc.s[q]);
+              } else if constexpr (MODE == 1) {
+                // A4 (R7): fl32(fl32(code2[qabsmax] * absmax2) + offset), two roundings
+                const uint32_t qb = (sc.s[0] >> (8 * q)) & 0xFFu;
+                const float a2 = ((b0 + q) >> 8) == (b0 >> 8) ? sc.a2[0] : sc.a2[1];
+                a = __fadd_rn(__fmul_rn(code2s[qb], a2), p.offset);
+              } else {
+                a = __fadd_rn(__fmul_rn(code2s[sc.s[q]], sc.a2[q]), p.offset);
+              }
+              const uint4 c0 = *reinterpret_cast<const uint4*>(smem_c + cs * kSuperCodeBytes +
+                                                               code_chunk_off<SUB>(t, 2 * q + half));
+              // dequantize 32 weights: word jj = (element 2jj) | (element 2jj+1) << 16
+              const uint32_t cw[4] = {c0.x, c0.y, c0.z, c0.w};
+              const uint64_t aa = f32x2_splat(a);
+#pragma unroll
+              for (int cc = 0; cc < 4; ++cc) {
+                const uint32_t x = cw[cc];
+                const uint32_t hi4 = (x >> 2) & 0x3C3C3C3Cu;  // byte jj = 4 * high nibble (LUT byte offset)
+                const uint32_t lo4 = (x << 2) & 0x3C3C3C3Cu;  // byte jj = 4 * low nibble
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                  // shared address of NF4[idx] = lut_base with byte 0 replaced by byte jj of hi4/lo4: one PRMT
+                  const uint32_t ah = __byte_perm(hi4, lut_base, 0x7650u + jj);
+                  const uint32_t al = __byte_perm(lo4, lut_base, 0x7650u + jj);
+                  float ch, cl;
+                  asm("ld.shared.f32 %0, [%1];" : "=f"(ch) : "r"(ah));
+                  asm("ld.shared.f32 %0, [%1];" : "=f"(cl) : "r"(al));
+                  mul2_rn(ch, cl, aa);                      // fl32(NF4[idx] * a) for both, one FMUL2
+                  w[4 * cc + jj] = pack2_rn<BF16>(ch, cl);
+                }
+              }
+            }
+            if (!NF4_EXP(4)) {
+              // 16 columns (32 weights) of this row's A tile (group g, chunk q) in TMEM
+              const uint32_t taddr = tmem + tlane + uint32_t(A0 + (g * SUB + q) * 32 + half * 16);
+              asm volatile(
+                  "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+                  ::"r"(taddr), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]),
+                  "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]), "r"(w[15])
+                  : "memory");
+            }
+          }
+        };
+        using T_ = std::true_type;
+        using F_ = std::false_type;
+        const bool full = (j + 1) * SUB <= nk;
+        if (p.absmax != nullptr) {
+          if (full) stage(T_{}, std::integral_constant<int, 0>{}); else stage(F_{}, std::integral_constant<int, 0>{});
+        } else if (fast) {
+          if (full) stage(T_{}, std::integral_constant<int, 1>{}); else stage(F_{}, std::integral_constant<int, 1>{});
+        } else {
+          if (full) stage(T_{}, std::integral_constant<int, 2>{}); else stage(F_{}, std::integral_constant<int, 2>{});
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (wl == 0 && lane == 0) NF4_TRACE_J(300, Jg);
+        if (lane == 0) mbar_arrive(&w_full[g]);      // A tiles written, codes read
       }
+
+      // ======================= epilogue (the group of the segment's last super-stage) =======================
+      const int jlast = J + (nsuper > 0 ? nsuper - 1 : 0);
+      if (jlast % G == g) {
+        const int ab = sidx % NACC;
+        mbar_wait_parity(&acc_full[ab], uint32_t(sidx / NACC) & 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int qd = wl & 3;                           // TMEM lane quarter this warp may access
+        constexpr int HB = BN / 2 < 16 ? 16 : BN / 2;    // columns per warp (BN = 16: warps 4-7 idle)
+        const int col0 = half * HB;
+        const int n = sg.n0 + qd * 32 + lane;
+        const uint32_t taddr = tmem + (uint32_t(qd * 32) << 16) + uint32_t(ab * ACC);
+        const bool direct = p.streamk ? (sg.kc0 == 0 && nk == p.nk) : p.splits == 1;
+#pragma unroll 1
+        for (int cb = col0; cb < col0 + HB && cb < BN; cb += 16) {
+          uint32_t v[16];
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+              : "r"(taddr + cb));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (n < p.N) {
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) {
+              const int m = sg.m0 + cb + jj;
+              if (m < p.M) {
+                const float acc = nk > 0 ? __uint_as_float(v[jj]) : 0.0f;
+                if (!direct) {
+                  p.partial[(int64_t(sg.part) * p.M + m) * p.N + n] = acc;
+                } else if (p.out_dtype == NF4_F32) {
+                  static_cast<float*>(p.y)[int64_t(m) * p.N + n] = acc;
+                } else {
+                  static_cast<uint16_t*>(p.y)[int64_t(m) * p.N + n] =
+                      p.out_dtype == NF4_BF16 ? cvt1_rn<true>(acc) : cvt1_rn<false>(acc);
+                }
+              }
+            }
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[ab]);     // the MMA may reuse this accumulator
+        if (p.streamk && !direct && sg.kc0 + nk < p.nk) {
+          // a non-final piece: publish (release) -- the tile's last CTA sums it at its end
+          __threadfence();
+          __syncwarp();
+          if (lane == 0) atomicAdd(p.flags + (sg.m0 / BN) * p.tiles_n + sg.n0 / 128, 1u);
+        }
+        if (NF4_TRACING && threadIdx.x == 32 * 8 * g) p.trace[1024 + 4 * cta_lin + 3] = gtimer();
+      }
+      J += nsuper;
+      ++sidx;
     }
-  } else if (warp == kProducerWarps + 1) {
+  } else if (warp == kTmaWarp) {
     // ======================= TMA issuer (one thread) =======================
     if (lane == 0) {
-      for (int i = 0; i < nk; ++i) {
-        const int s = i % STAGES;
-        mbar_wait_parity(&empty[s], ((i / STAGES) & 1) ^ 1);   // MMA of chunk i-STAGES released the slot
-        const int k0 = (kc0 + i) * kChunk;
-        asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
-            smem_u32(&tma_full[s])), "r"(kStageTx) : "memory");
-        tma_load_2d(smem_c + s * 128 * kCodeBytes, &map_codes, k0 / 2, n0, &tma_full[s]);
-        tma_load_2d(smem_x + s * BN * kRowBytes, &map_x, k0, m0, &tma_full[s]);
-      }
-    }
-  } else if (lane == 0) {
-    // ======================= MMA issuer (one thread) =======================
-    const uint32_t idesc = umma_idesc(BN, BF16);
-    for (int i = 0; i < nk; ++i) {
-      const int s = i % STAGES;
-      mbar_wait_parity(&tma_full[s], (i / STAGES) & 1);
-      mbar_wait_parity(&w_full[s], (i / STAGES) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t xa = smem_u32(smem_x + s * BN * kRowBytes);
+      int J = 0;
+      SegIter it = seg_begin(sk_range);
+      Segment sg;
+      while (next_segment<BN>(p, it, sg)) {
+        const int nsuper = (sg.nk + SUB - 1) / SUB;
+        for (int j = 0; j < nsuper; ++j) {
+          const int Jg = J + j, cs = Jg % CST;
+          mbar_wait_parity(&c_free[cs], (uint32_t(Jg / CST) & 1u) ^ 1u);   // super-stage Jg-CST consumed
+          NF4_TRACE_J(400, Jg);
+          const int k0 = (sg.kc0 + j * SUB) * kChunk;
+          const bool ld_c = !(NF4_EXP(16)), ld_x = !(NF4_EXP(8));
+          asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
+              smem_u32(&c_full[cs])), "r"(uint32_t((ld_c ? kSuperCodeBytes : 0) + (ld_x ? kSuperXBytes : 0))) : "memory");
+          if (ld_c) tma_load_2d(smem_c + cs * kSuperCodeBytes, &map_codes, k0 / 2, sg.n0, &c_full[cs]);
+          if (ld_x) {
 #pragma unroll
-      for (int kk = 0; kk < kChunk / 16; ++kk) {
-        const uint32_t a_tmem = tmem + uint32_t(ACC_COLS + s * 32 + kk * 8);   // A: 128 lanes x 16 weights
-        const uint64_t bdesc = umma_desc_sw128(xa + kk * 32);
-        const uint32_t accum = (i > 0 || kk > 0) ? 1u : 0u;
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "setp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}"
-            ::"r"(tmem), "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accum) : "memory");
+            for (int q = 0; q < SUB; ++q)
+              tma_load_2d(smem_x + cs * kSuperXBytes + q * BN * kRowBytes, &map_x, k0 + q * kChunk, sg.m0,
+                          &c_full[cs]);
+          }
+        }
+        J += nsuper;
       }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-          smem_u32(&empty[s])) : "memory");
     }
-    if (nk > 0)
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-          smem_u32(done)) : "memory");
-    else
-      mbar_arrive(done);
+  } else {
+    // ======================= MMA issuer (whole warp, one elected lane issues) =======================
+    const uint32_t idesc = umma_idesc(BN, BF16);
+    int J = 0, sidx = 0;
+    SegIter it = seg_begin(sk_range);
+    Segment sg;
+    while (next_segment<BN>(p, it, sg)) {
+      const int nsuper = (sg.nk + SUB - 1) / SUB;
+      const int ab = sidx % NACC;
+      mbar_wait_parity(&acc_empty[ab], (uint32_t(sidx / NACC) & 1u) ^ 1u);   // its previous epilogue done
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t d_tmem = tmem + uint32_t(ab * ACC);
+      for (int j = 0; j < nsuper; ++j) {
+        const int Jg = J + j, g = Jg % G, cs = Jg % CST;
+        mbar_wait_parity(&w_full[g], uint32_t(Jg / G) & 1u);               // A tiles in TMEM (X landed before)
+        if (lane == 0) NF4_TRACE_J(500, Jg);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (!(NF4_EXP(1))) {
+          const uint64_t b0 = umma_desc_sw128(smem_u32(smem_x + cs * kSuperXBytes));
+          const uint32_t a0 = tmem + uint32_t(A0 + g * SUB * 32);
+#pragma unroll
+          for (int q = 0; q < SUB; ++q) {
+            if (j * SUB + q < sg.nk)
+              umma_chunk_elect(d_tmem, a0 + q * 32, b0 + uint64_t(q * BN * kRowBytes / 16), idesc,
+                               (j > 0 || q > 0) ? 1u : 0u);
+          }
+        }
+        umma_commit_elect(&a_free[g]);
+        umma_commit_elect(&c_free[cs]);
+      }
+      if (nsuper > 0)
+        umma_commit_elect(&acc_full[ab]);
+      else if (lane == 0)
+        mbar_arrive(&acc_full[ab]);
+      J += nsuper;
+      ++sidx;
+    }
+    __syncwarp();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == kProducerWarps) {
+  if (p.streamk) {
+    // ======================= stream-K fix-up of the tile this range finishes =======================
+    const int x0 = sk_range[0], tile = x0 / p.nk, kc0 = x0 - tile * p.nk, parts = sk_range[2] + 1;
+    if (kc0 > 0 && sk_range[1] >= (tile + 1) * p.nk) {
+      unsigned* flag = p.flags + tile;
+      if (threadIdx.x == 0) {
+        const unsigned want = unsigned(kProducerWarps * (parts - 1));
+        unsigned v;
+        while (true) {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+          if (v >= want) break;
+          __nanosleep(64);
+        }
+        *flag = 0u;                                   // leave the workspace clean for the next call
+      }
+      __syncthreads();
+      const int n0 = (tile % p.tiles_n) * 128, m0 = (tile / p.tiles_n) * BN;
+      const int rows = min(BN, p.M - m0);
+      const int64_t mn = int64_t(p.M) * p.N;
+      for (int e = threadIdx.x; e < rows * 128; e += blockDim.x) {
+        const int m = m0 + (e >> 7), n = n0 + (e & 127);
+        if (n >= p.N) continue;
+        const int64_t i = int64_t(m) * p.N + n;
+        float acc = __ldcg(p.partial + i);
+        for (int s2 = 1; s2 < parts; ++s2) acc = __fadd_rn(acc, __ldcg(p.partial + s2 * mn + i));
+        if (p.out_dtype == NF4_F32)
+          static_cast<float*>(p.y)[i] = acc;
+        else
+          static_cast<uint16_t*>(p.y)[i] = p.out_dtype == NF4_BF16 ? cvt1_rn<true>(acc) : cvt1_rn<false>(acc);
+      }
+    }
+  }
+  if (NF4_TRACING && threadIdx.x == 0) p.trace[1024 + 4 * cta_lin + 1] = gtimer();
+  if (warp == kMmaWarp) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
 }
 
-// Deterministic split-K reduction: y[m, n] = sum_s partial[s, m, n] in split order.
+// Deterministic reductions of the fp32 partials.
+// classic: y[m, n] = sum_s partial[s, m, n] in split order.
 __global__ void nf4_gemm_reduce_kernel(const float* __restrict__ partial, int splits, int64_t mn, void* y,
                                        int out_dtype) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < mn; i += int64_t(gridDim.x) * blockDim.x) {
@@ -350,32 +686,39 @@ __global__ void nf4_gemm_reduce_kernel(const float* __restrict__ partial, int sp
       static_cast<uint16_t*>(y)[i] = out_dtype == NF4_BF16 ? cvt1_rn<true>(acc) : cvt1_rn<false>(acc);
   }
 }
-
-template <int BN>
-constexpr int stages_for() {
-  // TMEM: accumulator + STAGES x 32 columns; BN <= 32 -> 128 columns -> 4 CTAs/SM fit in 512
-  return BN <= 32 ? 3 : BN <= 64 ? 6 : BN <= 128 ? 4 : 5;
-}
-template <int BN>
-constexpr int ring_for() {
-  return BN <= 64 ? 4 : 2;
-}
+// Per token-tile width: G producer groups, SUB chunks per super-stage (code box
+// width SUB*32 B), CST super-stages in shared memory, NACC accumulators in TMEM.
+//   BN 16: 24 KB x 6;  BN 32: 32 KB x 6;  BN 64: 48 KB x 4;  BN 128: 40 KB x 4;
+//   BN 256: 36 KB x 5 (one accumulator: 256 + 3*32 TMEM columns)
+constexpr int kGroups = 3;
+template <int BN> constexpr int sub_for() { return BN <= 64 ? 4 : BN <= 128 ? 2 : 1; }
+#ifndef NF4_GEMM_CST_SMALL
+#define NF4_GEMM_CST_SMALL 6
+#endif
+template <int BN> constexpr int cst_for() { return BN <= 16 ? NF4_GEMM_CST_SMALL : BN <= 32 ? 6 : BN <= 128 ? 4 : 5; }
+template <int BN> constexpr int nacc_for() { return BN <= 128 ? 2 : 1; }
+constexpr int threads_for() { return 32 * (8 * kGroups + 2); }
 
 template <int BN>
 constexpr size_t smem_bytes() {
-  return 1024 /*align slack*/ + size_t(stages_for<BN>()) * (BN * kRowBytes + 128 * kCodeBytes) +
-         (3 * stages_for<BN>() + 1) * 8 + 16 + 64 + 1024 + 64;
+  return 1024 /*align slack*/ + size_t(cst_for<BN>()) * sub_for<BN>() * (128 * kCodeBytes + BN * kRowBytes);
+}
+
+template <int BN, bool BF16>
+constexpr auto kernel_for() {
+  return nf4_gemm_kernel<BN, kGroups, sub_for<BN>(), cst_for<BN>(), nacc_for<BN>(), BF16>;
 }
 
 template <int BN, bool BF16>
 static cudaError_t launch(const GemmParams& p, const CUtensorMap& mc, const CUtensorMap& mx, dim3 grid,
                           cudaStream_t s) {
-  constexpr int ST = stages_for<BN>();
-  auto k = nf4_gemm_kernel<BN, ST, ring_for<BN>(), BF16>;
+  auto k = kernel_for<BN, BF16>();
   constexpr size_t sm = smem_bytes<BN>();
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-  if (e != cudaSuccess) return e;
-  k<<<grid, kThreads, sm, s>>>(p, mc, mx);
+  static std::once_flag once;          // per instantiation (per process: one device type)
+  static cudaError_t attr = cudaSuccess;
+  std::call_once(once, [&] { attr = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)); });
+  if (attr != cudaSuccess) return attr;
+  k<<<grid, threads_for(), sm, s>>>(p, mc, mx);
   return cudaPeekAtLastError();
 }
 
@@ -396,17 +739,42 @@ static EncodeTiledFn encoder() {
   return fn;
 }
 
-// 2-D tensor map over a row-major [rows, cols] matrix of `elem` bytes.
+// L2 promotion of the TMA requests (none / 64B / 128B measured the same, r01).
+static CUtensorMapL2promotion promo() { return CU_TENSOR_MAP_L2_PROMOTION_L2_256B; }
+
+// 2-D tensor map over a row-major [rows, cols] matrix of `elem` bytes.  The last
+// encodings are cached per host thread (a decode step re-issues the same weights).
 static bool make_map(CUtensorMap* m, CUtensorMapDataType dt, int elem, const void* base, uint64_t cols,
                      uint64_t rows, uint32_t box_cols, uint32_t box_rows, CUtensorMapSwizzle sw) {
+  struct Entry {
+    const void* base;
+    uint64_t cols, rows;
+    uint32_t box_cols, box_rows;
+    int dt, sw;
+    CUtensorMap map;
+  };
+  constexpr int kCache = 64;
+  thread_local Entry cache[kCache] = {};
+  const uint64_t h = (reinterpret_cast<uintptr_t>(base) >> 8) ^ (cols * 0x9E3779B97F4A7C15ull) ^ (rows << 7) ^
+                     (uint64_t(box_rows) << 3) ^ uint64_t(dt);
+  Entry& c = cache[(h ^ (h >> 29)) % kCache];
+  if (c.base == base && c.cols == cols && c.rows == rows && c.box_cols == box_cols && c.box_rows == box_rows &&
+      c.dt == int(dt) && c.sw == int(sw)) {
+    *m = c.map;
+    return true;
+  }
   EncodeTiledFn enc = encoder();
   if (!enc) return false;
   const cuuint64_t dims[2] = {cols, rows};
   const cuuint64_t strides[1] = {cols * uint64_t(elem)};
   const cuuint32_t box[2] = {box_cols, box_rows};
   const cuuint32_t estr[2] = {1, 1};
-  return enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
-             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  if (enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+          promo(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  c.base = base; c.cols = cols; c.rows = rows; c.box_cols = box_cols; c.box_rows = box_rows;
+  c.dt = int(dt); c.sw = int(sw); c.map = *m;
+  return true;
 }
 
 }  // namespace gemm
@@ -423,32 +791,51 @@ static int pick_bn(int M) {
   return 256;
 }
 
+// Stream-K geometry: G resident CTAs (at most one per 4 chunks so every range
+// is non-empty), W chunks in total, and the largest number of segments any
+// tile is split into (= partial slots the workspace needs).
+struct SkGeom {
+  int bn, tiles_n, tiles_m, nk, align4;
+  int64_t W, G;
+  int max_parts;
+};
+static SkGeom sk_geometry(int M, int N, int K) {
+  SkGeom g;
+  g.bn = pick_bn(M);
+  g.tiles_n = (N + 127) / 128;
+  g.tiles_m = (M + g.bn - 1) / g.bn;
+  g.nk = K / 64;
+  g.align4 = (g.nk % 4) == 0;
+  g.W = int64_t(g.tiles_n) * g.tiles_m * g.nk;
+  const int64_t cap = sm_count();   // one CTA per SM (the kernel's 3 producer groups fill it)
+  const int64_t lim = g.align4 ? g.W / 4 : g.W;
+  g.G = cap < lim ? cap : lim;
+  if (g.G < 1) g.G = 1;
+  // Upper bound on the pieces of one tile (sizes the workspace; O(1) on the host):
+  // every range but the first touching a tile holds >= Lmin of its chunks.
+  int64_t lmin = g.W / g.G - (g.align4 ? 4 : 0);
+  if (lmin < (g.align4 ? 4 : 1)) lmin = g.align4 ? 4 : 1;
+  int64_t mp = 1 + (g.nk - 1 + lmin - 1) / lmin;
+  if (mp > g.G) mp = g.G;
+  g.max_parts = int(mp);
+  return g;
+}
+
+// stream-K workspace: per-tile counters (zero between calls), then the partials
+static int64_t sk_flag_bytes(const SkGeom& g) {
+  return (int64_t(g.tiles_n) * g.tiles_m * 4 + 255) / 256 * 256;
+}
+
 extern "C" int64_t nf4_gemm_workspace_bytes(int32_t M, int32_t N, int32_t K, int32_t splits) {
-  if (M <= 0 || N <= 0 || K <= 0 || splits <= 1) return 0;
+  if (M <= 0 || N <= 0 || K <= 0) return 0;
+  if (splits <= 0) {
+    if (K % 64 != 0) return 0;
+    const SkGeom g = sk_geometry(M, N, K);
+    if (g.W >= (int64_t(1) << 31)) return nf4_gemm_workspace_bytes(M, N, K, nf4_gemm_default_splits(M, N, K));
+    return g.max_parts > 1 ? sk_flag_bytes(g) + int64_t(g.max_parts) * M * N * 4 : 0;
+  }
+  if (splits <= 1) return 0;
   return int64_t(splits) * M * N * 4;
-}
-
-template <int BN, bool BF16>
-static int gemm_occupancy() {
-  static int occ = 0;
-  if (occ == 0) {
-    int v = 0;
-    auto k = nf4_gemm_kernel<BN, stages_for<BN>(), ring_for<BN>(), BF16>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_bytes<BN>()));
-    occ = (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, kThreads, smem_bytes<BN>()) == cudaSuccess && v > 0)
-              ? v : 1;
-  }
-  return occ;
-}
-
-static int occupancy_for_bn(int bn) {
-  switch (bn) {
-    case 16: return gemm_occupancy<16, true>();
-    case 32: return gemm_occupancy<32, true>();
-    case 64: return gemm_occupancy<64, true>();
-    case 128: return gemm_occupancy<128, true>();
-    default: return gemm_occupancy<256, true>();
-  }
 }
 
 // Split-K factor minimising the makespan of the (row tile, token tile, split)
@@ -458,7 +845,7 @@ extern "C" int32_t nf4_gemm_default_splits(int32_t M, int32_t N, int32_t K) {
   if (M <= 0 || N <= 0 || K <= 0) return 1;
   const int bn = pick_bn(M);
   const int64_t tiles = int64_t((N + 127) / 128) * ((M + bn - 1) / bn);
-  const int64_t cap = int64_t(sm_count()) * occupancy_for_bn(bn);
+  const int64_t cap = sm_count();
   const int64_t nk = K / 64;
   int best_s = 1;
   double best = 1e30;
@@ -490,13 +877,28 @@ extern "C" nf4_status nf4_gemm(const void* x, nf4_dtype x_dtype, int32_t M, cons
   if (!aligned(x, 16) || !aligned(packed, 16)) return NF4_ERR_MISALIGNED;
   if (!aligned(y, y_dtype == NF4_F32 ? 4 : 2)) return NF4_ERR_MISALIGNED;
   if (absmax && !aligned(absmax, 4)) return NF4_ERR_MISALIGNED;
-  if (splits <= 0) splits = nf4_gemm_default_splits(M, N, K);
   const int nk = K / 64;
-  if (splits > nk) splits = nk > 0 ? nk : 1;
-  if (splits > 1) {
-    if (!workspace) return NF4_ERR_NULL_POINTER;
-    if (workspace_bytes < nf4_gemm_workspace_bytes(M, N, K, splits)) return NF4_ERR_BAD_STATE;
-    if (!aligned(workspace, 16)) return NF4_ERR_MISALIGNED;
+  // stream-K chunk indices are 32-bit in the kernel; beyond that, the classic grid
+  const int64_t w_chunks = int64_t((N + 127) / 128) * ((M + pick_bn(M) - 1) / pick_bn(M)) * nk;
+  const bool streamk = splits <= 0 && nk > 0 && w_chunks < (int64_t(1) << 31);
+  if (splits <= 0 && !streamk) splits = nf4_gemm_default_splits(M, N, K);
+  SkGeom g{};
+  if (streamk) {
+    g = sk_geometry(M, N, K);
+    if (g.max_parts > 1) {
+      if (!workspace) return NF4_ERR_NULL_POINTER;
+      if (workspace_bytes < sk_flag_bytes(g) + int64_t(g.max_parts) * M * N * 4) return NF4_ERR_BAD_STATE;
+      if (!aligned(workspace, 16)) return NF4_ERR_MISALIGNED;
+    }
+    splits = 1;
+  } else {
+    if (splits <= 0) splits = 1;
+    if (splits > nk) splits = nk > 0 ? nk : 1;
+    if (splits > 1) {
+      if (!workspace) return NF4_ERR_NULL_POINTER;
+      if (workspace_bytes < nf4_gemm_workspace_bytes(M, N, K, splits)) return NF4_ERR_BAD_STATE;
+      if (!aligned(workspace, 16)) return NF4_ERR_MISALIGNED;
+    }
   }
   GemmParams p;
   p.packed = packed;
@@ -508,21 +910,49 @@ extern "C" nf4_status nf4_gemm(const void* x, nf4_dtype x_dtype, int32_t M, cons
   p.x = static_cast<const uint16_t*>(x);
   p.y = y;
   p.partial = static_cast<float*>(workspace);
+  p.flags = nullptr;
+  if (streamk && g.max_parts > 1) {
+    p.flags = static_cast<unsigned*>(workspace);
+    p.partial = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + sk_flag_bytes(g));
+  }
   p.M = M;
   p.N = N;
   p.K = K;
   p.bs_shift = log2i(blocksize);
+  {
+    // whole super-stages per split (SUB chunks share one TMA box); splits = non-empty ranges
+    const int bn0 = pick_bn(M);
+    const int sub = bn0 <= 64 ? 4 : bn0 <= 128 ? 2 : 1;
+    int cps = (nk + splits - 1) / splits;
+    cps = (cps + sub - 1) / sub * sub;
+    splits = (nk + cps - 1) / cps;
+    p.chunks_per_split = cps;
+  }
   p.splits = splits;
-  p.chunks_per_split = (nk + splits - 1) / splits;
   p.out_dtype = int(y_dtype);
+  p.streamk = streamk ? 1 : 0;
+  p.tiles_n = (N + 127) / 128;
+  p.tiles_m = (M + pick_bn(M) - 1) / pick_bn(M);
+  p.nk = nk;
+  p.total_chunks = int64_t(p.tiles_n) * p.tiles_m * nk;
+  p.align4 = streamk ? g.align4 : 0;
+  p.trace = nullptr;
+  p.experiment = 0;
+#if NF4_GEMM_DIAG
+  if (const char* tr = getenv("NF4_GEMM_TRACE")) p.trace = reinterpret_cast<unsigned long long*>(strtoull(tr, 0, 0));
+  if (const char* ex = getenv("NF4_GEMM_EXPERIMENT")) p.experiment = atoi(ex);
+#endif
   nf4_codebook(p.lut);
   const int bn = pick_bn(M);
-  dim3 grid((N + 127) / 128, (M + bn - 1) / bn, splits);
+  dim3 grid = streamk ? dim3(unsigned(g.G), 1, 1) : dim3((N + 127) / 128, (M + bn - 1) / bn, splits);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool bf16 = x_dtype == NF4_BF16;
   CUtensorMap mc, mx;
-  if (!make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, packed, uint64_t(K) / 2, uint64_t(N), kCodeBytes, 128,
-                CU_TENSOR_MAP_SWIZZLE_NONE) ||
+  const int sub = bn <= 64 ? 4 : bn <= 128 ? 2 : 1;
+  const CUtensorMapSwizzle csw = sub == 4 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                 : sub == 2 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
+  if (!make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, packed, uint64_t(K) / 2, uint64_t(N), uint32_t(sub * kCodeBytes),
+                128, csw) ||
       !make_map(&mx, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, x, uint64_t(K),
                 uint64_t(M), kChunk, uint32_t(bn), CU_TENSOR_MAP_SWIZZLE_128B))
     return NF4_ERR_CUDA;
@@ -536,7 +966,7 @@ extern "C" nf4_status nf4_gemm(const void* x, nf4_dtype x_dtype, int32_t M, cons
   }
   if (e != cudaSuccess) { cudaGetLastError(); return NF4_ERR_CUDA; }
   int launches = 1;
-  if (splits > 1) {
+  if (!streamk && splits > 1) {
     const int64_t mn = int64_t(M) * N;
     int64_t g = (mn + 255) / 256;
     if (g > int64_t(sm_count()) * 8) g = int64_t(sm_count()) * 8;

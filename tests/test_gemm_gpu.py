@@ -61,7 +61,11 @@ def _run(nf4, x16, xdt, M, packed, kw, N, K, bs, ydt, splits):
 @pytest.mark.parametrize("dq", [False, True])
 def test_gemm_weights_bit_exact_via_one_hot(nf4, orc, xdt, dq):
     """Y[m, n] = W[n, k_m] exactly: the tensor cores saw the hot path's weights."""
-    for (M, N, K, bs, splits) in ((16, 256, 512, 64, 1), (5, 384, 1024, 128, 3), (40, 200, 640, 64, 2)):
+    # splits 0 = stream-K: (16, 5120, 448) has 7 chunks per tile (ranges not 4-aligned,
+    # tiles cut into up to 7 segments); (300, 256, 1280) two token tiles, 5 segments each
+    cases = ((16, 256, 512, 64, 1), (5, 384, 1024, 128, 3), (40, 200, 640, 64, 2),
+             (16, 256, 512, 64, 0), (40, 200, 640, 64, 0), (16, 5120, 448, 64, 0), (300, 256, 1280, 64, 0))
+    for (M, N, K, bs, splits) in cases:
         packed, kw = _weights(N, K, bs, dq, seed=M + N + K)
         ks = (np.arange(M) * 37 + 11) % K
         x = np.zeros((M, K), np.float32)
@@ -72,7 +76,7 @@ def test_gemm_weights_bit_exact_via_one_hot(nf4, orc, xdt, dq):
         w16 = orc.dequantize(packed, N * K, bs, code, threads=8, **kw).reshape(N, K)
         np16 = ml_dtypes.bfloat16 if xdt == "bf16" else np.float16
         want = w16[:, ks].T.view(np16).astype(np.float32)           # [M, N]
-        assert np.array_equal(y.view(np.uint32), want.view(np.uint32)), (M, N, K)
+        assert np.array_equal(y.view(np.uint32), want.view(np.uint32)), (M, N, K, splits)
 
 
 SHAPES = [(1, 128, 64), (2, 256, 1024), (7, 384, 2048), (16, 1024, 4096), (33, 640, 1536),
@@ -113,6 +117,41 @@ def test_gemm_split_k_is_deterministic(nf4):
     a = _run(nf4, x16, "bf16", M, packed, kw, N, K, 64, "f32", 4).cpu().numpy()
     b = _run(nf4, x16, "bf16", M, packed, kw, N, K, 64, "f32", 4).cpu().numpy()
     assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def test_gemm_stream_k_is_deterministic_and_matches_classic(nf4, orc):
+    """Stream-K: identical bits run to run; within the fp32 bound of the oracle."""
+    M, N, K = 16, 21504 // 8, 5376
+    rng = np.random.Generator(np.random.Philox(9))
+    x16 = rng.standard_normal((M, K)).astype(np.float32).astype(ml_dtypes.bfloat16).view(np.uint16)
+    packed, kw = _weights(N, K, 64, True, 4)
+    a = _run(nf4, x16, "bf16", M, packed, kw, N, K, 64, "f32", 0).cpu().numpy()
+    b = _run(nf4, x16, "bf16", M, packed, kw, N, K, 64, "f32", 0).cpu().numpy()
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    ref, mag = orc.gemm_reference(x16, orc.OUT_BF16, packed, N, K, 64, **kw)
+    assert (np.abs(a.astype(np.float64) - ref) <= K * 2.0 ** -23 * mag + 1e-30).all()
+
+
+def test_gemm_stream_k_workspace_reuse(nf4, orc):
+    """One zero-filled workspace serves a sequence of stream-K calls of different
+    shapes (each call leaves its per-tile counters at zero again)."""
+    import torch
+    shapes = [(16, 5120, 448), (16, 21504 // 8, 5376), (40, 2048, 1024), (16, 5120, 448)]
+    need = max(nf4.nf4_gemm_workspace_bytes(M, N, K, 0) for M, N, K in shapes)
+    assert need > 0
+    ws = torch.zeros(need, dtype=torch.uint8, device="cuda")
+    for idx, (M, N, K) in enumerate(shapes):
+        rng = np.random.Generator(np.random.Philox(100 + idx))
+        x16 = rng.standard_normal((M, K)).astype(np.float32).astype(ml_dtypes.bfloat16).view(np.uint16)
+        packed, kw = _weights(N, K, 64, False, 50 + idx)
+        x = dev(x16.view(np.int16)).view(torch.bfloat16).reshape(M, K)
+        y = nf4.nf4_gemm(x, dev(packed), dev(kw["absmax"]), None, N=N, K=K, y_dtype="f32", workspace=ws)
+        torch.cuda.synchronize()
+        ref, mag = orc.gemm_reference(x16, orc.OUT_BF16, packed, N, K, 64, **kw)
+        err = np.abs(y.cpu().numpy().astype(np.float64) - ref)
+        assert (err <= K * 2.0 ** -23 * mag + 1e-30).all(), (M, N, K)
+        tiles = -(-N // 128) * -(-M // (16 if M <= 16 else 32 if M <= 32 else 64 if M <= 64 else 128))
+        assert int(ws[:4 * tiles].view(torch.int32).abs().sum()) == 0, "stream-K counters not reset"
 
 
 def test_gemm_argument_errors(nf4):

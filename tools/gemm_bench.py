@@ -36,7 +36,8 @@ def main():
     ap.add_argument("--layers", type=int, default=None)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--splits", type=int, default=0)
+    ap.add_argument("--splits", type=int, default=0,
+                    help="0: stream-K (default); -1: classic grid, makespan split heuristic; >0: classic, fixed")
     ap.add_argument("--no-unfused", action="store_true")
     args = ap.parse_args()
 
@@ -60,10 +61,10 @@ def main():
     for t in tensors:
         key = (t.rows, t.cols)
         if key not in splits:
-            s = args.splits or nf4.nf4_gemm_default_splits(M, t.rows, t.cols)
+            s = nf4.nf4_gemm_default_splits(M, t.rows, t.cols) if args.splits < 0 else args.splits
             splits[key] = s
             b = nf4.nf4_gemm_workspace_bytes(M, t.rows, t.cols, s)
-            wsp[key] = torch.empty(max(b, 16), dtype=torch.uint8, device="cuda")
+            wsp[key] = torch.zeros(max(b, 16), dtype=torch.uint8, device="cuda")
 
     def fused_step():
         for i, (t, e) in enumerate(zip(tensors, ws.entries)):

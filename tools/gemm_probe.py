@@ -16,8 +16,8 @@ dq = nf4.DQ(ws._ptr(ws.scales, e.scale_off), ws.code2.data_ptr(), ws._ptr(ws.gro
 x = torch.randn(M, K, device="cuda").to(torch.bfloat16)
 y = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
 res = {}
-for s in (1, 2, 4, 8, 16, 32):
-    wsp = torch.empty(max(16, nf4.nf4_gemm_workspace_bytes(M, N, K, s)), dtype=torch.uint8, device="cuda")
+for s in (0, 1, 2, 4, 8, 16, 32):
+    wsp = torch.zeros(max(16, nf4.nf4_gemm_workspace_bytes(M, N, K, s)), dtype=torch.uint8, device="cuda")
     f = lambda: nf4.nf4_gemm(x, ws._ptr(ws.codes, e.codes_off), None, dq, N=N, K=K, y=y, splits=s, workspace=wsp)
     for _ in range(3): f()
     torch.cuda.synchronize()
