@@ -332,9 +332,6 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
     p.trace[1024 + 4 * cta_lin + 2] = smid;
   }
   if (threadIdx.x < 16) lut[threadIdx.x] = p.lut[threadIdx.x];
-  if (p.absmax == nullptr) {
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) code2s[i] = p.code2[i];
-  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < CST; ++s) {
       mbar_init(&c_full[s], 1);
@@ -367,6 +364,14 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
   if (warp == kTmaWarp && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_codes)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_x)) : "memory");
+  }
+  // Programmatic dependent launch: the next kernel in the stream may start its own
+  // prologue as soon as our CTAs leave their SMs; everything above touches only
+  // parameters and on-chip state, so it overlaps the previous kernel's tail.
+  if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // inputs (and the workspace) are now ready
+  if (p.absmax == nullptr) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) code2s[i] = p.code2[i];
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -718,7 +723,20 @@ static cudaError_t launch(const GemmParams& p, const CUtensorMap& mc, const CUte
   static cudaError_t attr = cudaSuccess;
   std::call_once(once, [&] { attr = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)); });
   if (attr != cudaSuccess) return attr;
-  k<<<grid, threads_for(), sm, s>>>(p, mc, mx);
+  // launched with programmatic stream serialization (the kernel executes
+  // griddepcontrol.wait before reading any input)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(threads_for());
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, k, p, mc, mx);
+  if (e != cudaSuccess) return e;
   return cudaPeekAtLastError();
 }
 
