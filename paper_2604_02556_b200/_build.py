@@ -47,7 +47,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 def build_variant(name: str, defines: dict) -> str:
     """Diagnostics only (tools/): the same sources with extra -D macros, e.g.
-    NF4_GEMM_DIAG=1 (event traces / pipeline-skipping experiments), into
+    NF4_GEMM_DIAG=1 (event traces) or 2 (+ pipeline-skipping experiments), into
     <repo>/_variants/libnf4_<name>.so; load it with NF4_LIB=<path>."""
     out_dir = os.path.join(ROOT, "_variants")
     os.makedirs(out_dir, exist_ok=True)

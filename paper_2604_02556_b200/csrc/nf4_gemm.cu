@@ -228,11 +228,17 @@ __device__ __forceinline__ uint32_t code_chunk_off(int row, int c16) {
 }
 
 // Segment enumeration: every role walks the same sequence.  Stream-K ranges are
-// computed once per CTA by one thread; only a range's first segment can start
-// inside a tile, so every later segment is its tile's partial slot 0.
+// computed once per CTA by one thread.  A range is [tail piece of a tile] [whole
+// tiles] [head piece of a tile]; the head piece (chunk 0 of its tile onward) is
+// processed FIRST, so its partial is published early and the CTA finishing that
+// tile (whose tail piece is its own first segment) never waits at the end.
+// Only the range's first chunk can start inside a tile, so every other segment
+// is its tile's partial slot 0.
 struct SegIter {
-  int x, end, start;   // stream-K: global chunk cursor, range end, range start
-  int part0;           // slot of the first segment
+  int x, end;          // stream-K: cursor and end of the current run
+  int start, hs;       // range start; head-piece start (== range start: none)
+  int part0;           // slot of the segment starting at the range start
+  int phase;           // 0: head piece, 1: the rest
   int done_classic;
 };
 template <int BN>
@@ -248,7 +254,12 @@ __device__ __forceinline__ bool next_segment(const GemmParams& p, SegIter& it, S
     sg.part = blockIdx.z;
     return true;
   }
-  if (it.x >= it.end) return false;
+  if (it.x >= it.end) {
+    if (it.phase != 0 || it.hs == it.start) return false;
+    it.phase = 1;                 // head piece done: now [start, hs)
+    it.x = it.start;
+    it.end = it.hs;
+  }
   const int tile = it.x / p.nk;
   const int tstart = tile * p.nk;
   const int send = min(it.end, tstart + p.nk);
@@ -260,12 +271,23 @@ __device__ __forceinline__ bool next_segment(const GemmParams& p, SegIter& it, S
   it.x = send;
   return true;
 }
-__device__ __forceinline__ SegIter seg_begin(const int (&range)[3]) {
+__device__ __forceinline__ SegIter seg_begin(const GemmParams& p, const int (&range)[3]) {
   SegIter it;
   it.done_classic = 0;
-  it.start = it.x = range[0];
-  it.end = range[1];
+  it.start = range[0];
   it.part0 = range[2];
+  it.hs = it.start;
+  it.phase = 1;
+  it.x = range[0];
+  it.end = range[1];
+  if (p.streamk && range[1] > range[0]) {
+    const int tl = (range[1] - 1) / p.nk, tsl = tl * p.nk;
+    if (range[1] < tsl + p.nk && tsl > range[0]) {   // the range ends inside a tile it did not start in
+      it.hs = tsl;
+      it.phase = 0;
+      it.x = tsl;                                      // head piece [tsl, end) first
+    }
+  }
   return it;
 }
 
@@ -388,7 +410,7 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
     const uint32_t tlane = uint32_t(32 * (wl & 3)) << 16;
     const uint32_t lut_base = smem_u32(lut);   // low byte 0: PRMT splices a byte offset into it
     int J = 0, sidx = 0;                       // super-stages / segments before this segment
-    SegIter it = seg_begin(sk_range);
+    SegIter it = seg_begin(p, sk_range);
     Segment sg;
     while (next_segment<BN>(p, it, sg)) {
       const int row = sg.n0 + t;
@@ -575,7 +597,7 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
     // ======================= TMA issuer (one thread) =======================
     if (lane == 0) {
       int J = 0;
-      SegIter it = seg_begin(sk_range);
+      SegIter it = seg_begin(p, sk_range);
       Segment sg;
       while (next_segment<BN>(p, it, sg)) {
         const int nsuper = (sg.nk + SUB - 1) / SUB;
@@ -602,7 +624,7 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
     // ======================= MMA issuer (whole warp, one elected lane issues) =======================
     const uint32_t idesc = umma_idesc(BN, BF16);
     int J = 0, sidx = 0;
-    SegIter it = seg_begin(sk_range);
+    SegIter it = seg_begin(p, sk_range);
     Segment sg;
     while (next_segment<BN>(p, it, sg)) {
       const int nsuper = (sg.nk + SUB - 1) / SUB;

@@ -13,7 +13,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 if not os.environ.get("NF4_LIB"):   # event traces / experiments need the diagnostics build
     from paper_2604_02556_b200 import _build
-    os.environ["NF4_LIB"] = _build.build_variant("diag", {"NF4_GEMM_DIAG": 1})
+    os.environ["NF4_LIB"] = _build.build_variant("exp", {"NF4_GEMM_DIAG": 2})
 import torch
 
 import paper_2604_02556_b200 as nf4

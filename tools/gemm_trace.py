@@ -2,7 +2,7 @@ import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 if not os.environ.get("NF4_LIB"):   # event traces / experiments need the diagnostics build
     from paper_2604_02556_b200 import _build
-    os.environ["NF4_LIB"] = _build.build_variant("diag", {"NF4_GEMM_DIAG": 1})
+    os.environ["NF4_LIB"] = _build.build_variant("trace", {"NF4_GEMM_DIAG": 1})
 import torch
 import paper_2604_02556_b200 as nf4
 from paper_2604_02556_b200 import weights
@@ -49,3 +49,19 @@ print("per-SM mean p0/50/100:", np.percentile(per_sm[per_sm > 0], [0, 50, 100]).
 # within-SM spread
 spread = [dur[sm_ids == k].max() - dur[sm_ids == k].min() for k in set(sm_ids.tolist())]
 print("within-SM spread p50/max:", np.percentile(spread, [50, 100]).round(1))
+# slowest CTAs and their stream-K ranges (tile-major chunk stream, G = #CTAs)
+if S == 0:
+    nk = K // 64
+    bn = 16 if M <= 16 else 32 if M <= 32 else 64 if M <= 64 else 128 if M <= 128 else 256
+    tiles = -(-N // 128) * -(-M // bn)
+    W, G = tiles * nk, len(c)
+    a4 = nk % 4 == 0
+    def bnd(cc):
+        b = cc * W // G
+        if a4:
+            b = (b + 2) // 4 * 4
+        return min(b, W)
+    for idx in np.argsort(-dur)[:6]:
+        x0, x1 = bnd(idx), bnd(idx + 1)
+        print(f"CTA {idx}: {dur[idx]:.1f} us, start {st[idx]:.2f}, range [{x0},{x1}) tiles {x0 // nk}..{(x1 - 1) // nk}"
+              f" kc0 {x0 % nk} end-in-tile {x1 - (x1 - 1) // nk * nk}")
