@@ -17,7 +17,7 @@ from typing import Optional
 
 import torch
 
-from . import DQ, nf4_dequantize, nf4_double_quantize, nf4_gemm, nf4_quantize
+from . import DQ, nf4_dequantize, nf4_double_quantize, nf4_gemm, nf4_gemm_workspace_bytes, nf4_quantize
 
 
 class NF4Linear(torch.nn.Module):
@@ -44,6 +44,7 @@ class NF4Linear(torch.nn.Module):
             self.register_buffer("absmax", torch.zeros(nb, dtype=torch.float32, device=dev))
         self.bias: Optional[torch.Tensor] = None
         self._wbuf: Optional[torch.Tensor] = None
+        self._gemm_ws: dict = {}     # M -> zero-initialised stream-K workspace (kept zeroed by nf4_gemm)
 
     # ------------------------------------------------------------------ build
     @classmethod
@@ -90,8 +91,12 @@ class NF4Linear(torch.nn.Module):
         fused_ok = (K % 64 == 0 and K % self.blocksize == 0 and x2.data_ptr() % 16 == 0
                     and self.packed.data_ptr() % 16 == 0)
         if M <= self.fused_max_m and fused_ok:
+            ws = self._gemm_ws.get(M)
+            if ws is None:
+                nbytes = nf4_gemm_workspace_bytes(M, self.out_features, K, 0)
+                ws = self._gemm_ws[M] = torch.zeros(max(nbytes, 16), dtype=torch.uint8, device=x.device)
             y = nf4_gemm(x2, self.packed, self.absmax, self._dq(), N=self.out_features, K=K,
-                         blocksize=self.blocksize, y_dtype=self.compute_dtype)
+                         blocksize=self.blocksize, y_dtype=self.compute_dtype, workspace=ws)
         else:
             if self._wbuf is None or self._wbuf.numel() != self.in_features * self.out_features:
                 self._wbuf = torch.empty(self.in_features * self.out_features, dtype=self.compute_dtype,
