@@ -60,8 +60,25 @@ def main():
     x = torch.randn(3, 256, device="cuda").to(torch.bfloat16)
     wp = d(syn.hash_packed(9, 0, 128 * 256 // 2))
     wa = d(syn.hash_absmax(9, 0, 128 * 256 // 64))
-    for s in (1, 2):
+    for s in (1, 2, 0):
         nf4.nf4_gemm(x, wp, wa, None, N=128, K=256, splits=s)
+    # stream-K with tiles cut into several pieces (fix-up path), DQ scales, checked vs the oracle
+    M2, N2, K2 = 20, 2048, 1024
+    x2 = syn.gaussian_weights(M2 * K2, 2).reshape(M2, K2)
+    import ml_dtypes
+    x2_16 = x2.astype(ml_dtypes.bfloat16).view(np.uint16)
+    wp2 = syn.hash_packed(10, 0, N2 * K2 // 2)
+    nb2 = N2 * K2 // 64
+    kw2 = dict(qabsmax=syn.hash_qabsmax(10, 0, nb2), code2=code2, absmax2=syn.hash_absmax2(10, 0, -(-nb2 // 256)),
+               offset=float(syn.hash_offset(10)))
+    xt = d(x2_16.view(np.int16)).view(torch.bfloat16)
+    dqt = nf4.DQ(d(kw2["qabsmax"]), d(code2), d(kw2["absmax2"]), kw2["offset"])
+    ws2 = torch.zeros(max(16, nf4.nf4_gemm_workspace_bytes(M2, N2, K2, 0)), dtype=torch.uint8, device="cuda")
+    for _ in range(2):   # the second call reuses the (self-cleaning) workspace
+        y2 = nf4.nf4_gemm(xt, d(wp2), None, dqt, N=N2, K=K2, y_dtype="f32", workspace=ws2)
+    torch.cuda.synchronize()
+    ref2, mag2 = oracle.gemm_reference(x2_16, oracle.OUT_BF16, wp2, N2, K2, 64, **kw2)
+    bad += int(not (np.abs(y2.cpu().numpy().astype(np.float64) - ref2) <= K2 * 2.0 ** -23 * mag2 + 1e-30).all())
     # synth + sol
     buf8 = torch.empty(8192 * 4, dtype=torch.uint8, device="cuda")
     nf4.nf4_synth_fill(_lib.NF4_SYNTH_CODES, 1, 3, 1000, buf8)
