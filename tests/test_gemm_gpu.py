@@ -97,6 +97,52 @@ def test_gemm_random_within_fp32_bound(nf4, orc, M, N, K):
             assert (err <= bound).all(), (M, N, K, dq, splits, float((err / bound).max()))
 
 
+@pytest.mark.parametrize("bs", [64, 128, 256, 4096])
+@pytest.mark.parametrize("xdt", ["bf16", "f16"])
+def test_gemm_stream_k_blocksizes_and_dtypes(nf4, orc, bs, xdt):
+    """Stream-K (splits=0) on the general scale path (bs > 64), the fast one (bs 64),
+    fp16 and bf16 X, fp32 and double-quant absmax; K = 4096 keeps every blocksize legal
+    and cuts tiles into several pieces."""
+    M, N, K = 24, 1280, 4096
+    rng = np.random.Generator(np.random.Philox(bs + (xdt == "f16")))
+    xf = rng.standard_normal((M, K)).astype(np.float32)
+    x16 = (xf.astype(ml_dtypes.bfloat16) if xdt == "bf16" else xf.astype(np.float16)).view(np.uint16)
+    code = orc.OUT_BF16 if xdt == "bf16" else orc.OUT_F16
+    for dq in (False, True):
+        packed, kw = _weights(N, K, bs, dq, seed=bs + 7 * int(dq))
+        ref, mag = orc.gemm_reference(x16, code, packed, N, K, bs, **kw)
+        y = _run(nf4, x16, xdt, M, packed, kw, N, K, bs, "f32", 0).cpu().numpy().astype(np.float64)
+        err = np.abs(y - ref)
+        bound = K * 2.0 ** -23 * mag + 1e-30
+        assert (err <= bound).all(), (bs, xdt, dq, float((err / bound).max()))
+
+
+def test_gemm_stream_k_unaligned_scales_take_general_path(nf4, orc):
+    """absmax / qabsmax pointers that break the vector-load alignment of the fast
+    scale path must still give the same bits (general path)."""
+    import torch
+    M, N, K = 16, 512, 2048
+    rng = np.random.Generator(np.random.Philox(77))
+    x16 = rng.standard_normal((M, K)).astype(np.float32).astype(ml_dtypes.bfloat16).view(np.uint16)
+    x = dev(x16.view(np.int16)).view(torch.bfloat16).reshape(M, K)
+    packed, kw = _weights(N, K, 64, False, 12)
+    a_buf = torch.zeros(kw["absmax"].size + 1, dtype=torch.float32, device="cuda")
+    a_buf[1:] = dev(kw["absmax"])
+    y_al = nf4.nf4_gemm(x, dev(packed), dev(kw["absmax"]), None, N=N, K=K, y_dtype="f32")
+    y_un = nf4.nf4_gemm(x, dev(packed), a_buf[1:], None, N=N, K=K, y_dtype="f32")
+    torch.cuda.synchronize()
+    assert torch.equal(y_al.view(torch.int32), y_un.view(torch.int32))
+    packed, kw = _weights(N, K, 64, True, 13)
+    q_buf = torch.zeros(kw["qabsmax"].size + 1, dtype=torch.uint8, device="cuda")
+    q_buf[1:] = dev(kw["qabsmax"])
+    d_al = nf4.DQ(dev(kw["qabsmax"]), dev(kw["code2"]), dev(kw["absmax2"]), kw["offset"])
+    d_un = nf4.DQ(q_buf[1:], dev(kw["code2"]), dev(kw["absmax2"]), kw["offset"])
+    y_al = nf4.nf4_gemm(x, dev(packed), None, d_al, N=N, K=K, y_dtype="f32")
+    y_un = nf4.nf4_gemm(x, dev(packed), None, d_un, N=N, K=K, y_dtype="f32")
+    torch.cuda.synchronize()
+    assert torch.equal(y_al.view(torch.int32), y_un.view(torch.int32))
+
+
 def test_gemm_bf16_output_rounding(nf4, orc):
     M, N, K = 24, 384, 2048
     rng = np.random.Generator(np.random.Philox(5))
