@@ -52,6 +52,33 @@ nf4_status nf4_gemm(const void* x, nf4_dtype x_dtype, int32_t M, const uint8_t* 
 int32_t nf4_gemm_default_splits(int32_t M, int32_t N, int32_t K);
 int64_t nf4_gemm_workspace_bytes(int32_t M, int32_t N, int32_t K, int32_t splits);
 
+/*
+ * Grouped form: up to NF4_GEMM_MAX_GROUP weights that share the activation X
+ * (and K, blocksize) -- e.g. the q/k/v or gate/up projections of a decoder
+ * layer -- in ONE stream-K launch:  Y_i = X . W_i^T.  Each weight is described
+ * as for nf4_gemm (packed [N_i, K] codes, fp32 absmax or dq, its own y_i
+ * [M, N_i]); their 128-feature tiles are concatenated into one work stream, so
+ * the launch's fill/drain is paid once.  Numerics are nf4_gemm's (bit-exact
+ * weights, fp32 accumulation; the summation order can differ from separate
+ * calls).  workspace: nf4_gemm_grouped_workspace_bytes(M, N[], count, K) bytes,
+ * zero-filled before first use and left zeroed (same contract as stream-K
+ * nf4_gemm).  Errors: NF4_ERR_BAD_SIZE for count outside [1, 4] or a problem too
+ * large for the stream-K indices (> 2^31 chunk tiles), else as nf4_gemm.
+ */
+#define NF4_GEMM_MAX_GROUP 4
+typedef struct {
+  const uint8_t* packed;   /* [device] N*K/2 bytes, 16-byte aligned */
+  const float* absmax;     /* [device] fp32 absmax, or NULL for dq */
+  nf4_dq_state dq;         /* used when absmax == NULL */
+  int32_t N;               /* output features of this weight */
+  void* y;                 /* [device] M x N row-major, y_dtype */
+} nf4_gemm_weight;
+
+nf4_status nf4_gemm_grouped(const void* x, nf4_dtype x_dtype, int32_t M, int32_t K, int32_t blocksize,
+                            const nf4_gemm_weight* weights, int32_t count, nf4_dtype y_dtype, void* workspace,
+                            int64_t workspace_bytes, void* stream);
+int64_t nf4_gemm_grouped_workspace_bytes(int32_t M, const int32_t* N, int32_t count, int32_t K);
+
 #ifdef __cplusplus
 }
 #endif

@@ -28,6 +28,7 @@ __all__ = [
     "nf4_kernel_variants", "nf4_set_kernel_variant", "nf4_get_kernel_variant",
     "nf4_dequantize_ex", "nf4_dequantize_batched_ex", "nf4_codebook_fp4",
     "nf4_gemm", "nf4_gemm_default_splits", "nf4_gemm_workspace_bytes", "nf4_dequantize_host_batched",
+    "nf4_gemm_grouped", "nf4_gemm_grouped_workspace_bytes",
 ]
 
 
@@ -308,3 +309,39 @@ def nf4_gemm(x, packed, absmax=None, dq: Optional[DQ] = None, *, N: int, K: int,
                          _ptr(y), ycode, int(splits), _ptr(workspace), int(wsize), _stream(stream))
     _lib.check(st, "nf4_gemm")
     return y
+
+
+@functools.lru_cache(maxsize=4096)
+def nf4_gemm_grouped_workspace_bytes(M: int, Ns: tuple, K: int) -> int:
+    arr = (ctypes.c_int32 * len(Ns))(*[int(n) for n in Ns])
+    return int(load().nf4_gemm_grouped_workspace_bytes(int(M), arr, len(Ns), int(K)))
+
+
+def nf4_gemm_grouped(x, weights, *, K: int, blocksize: int = 64, ys=None, y_dtype="bf16", workspace=None,
+                     stream=None):
+    """Y_i = X . W_i^T for up to 4 NF4 weights sharing X (e.g. q/k/v) in one stream-K
+    launch (include/nf4_gemm.h).  weights: sequence of (packed, absmax, dq, N);
+    returns the list of y_i [M, N_i] (allocated with torch unless `ys` is given)."""
+    import torch
+    M = x.shape[0] if x.dim() == 2 else x.numel() // K
+    ycode = _dtype_code(y_dtype)
+    tdt = {_lib.NF4_F16: torch.float16, _lib.NF4_BF16: torch.bfloat16, _lib.NF4_F32: torch.float32}[ycode]
+    if ys is None:
+        ys = [torch.empty((M, int(w[3])), dtype=tdt, device=x.device) for w in weights]
+    Ns = tuple(int(w[3]) for w in weights)
+    wbytes = nf4_gemm_grouped_workspace_bytes(M, Ns, K)
+    if wbytes > 0 and workspace is None:
+        workspace = torch.zeros(wbytes, dtype=torch.uint8, device=x.device)
+    wsize = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    arr = (_lib.GemmWeight * len(weights))()
+    for i, (packed, absmax, dq, n) in enumerate(weights):
+        arr[i].packed = _ptr(packed)
+        arr[i].absmax = _ptr(absmax)
+        if dq is not None:
+            arr[i].dq = dq.c()
+        arr[i].N = int(n)
+        arr[i].y = _ptr(ys[i])
+    st = load().nf4_gemm_grouped(_ptr(x), _dtype_code(x.dtype), int(M), int(K), int(blocksize), arr, len(weights),
+                                 ycode, _ptr(workspace), int(wsize), _stream(stream))
+    _lib.check(st, "nf4_gemm_grouped")
+    return ys

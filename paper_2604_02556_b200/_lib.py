@@ -32,6 +32,7 @@ EXPORTS = [
     "nf4_kernel_variant_count", "nf4_kernel_variant_name", "nf4_set_kernel_variant", "nf4_get_kernel_variant",
     "nf4_dequantize_ex", "nf4_dequantize_batched_ex", "nf4_codebook_fp4",
     "nf4_gemm", "nf4_gemm_default_splits", "nf4_gemm_workspace_bytes", "nf4_dequantize_host_batched",
+    "nf4_gemm_grouped", "nf4_gemm_grouped_workspace_bytes",
 ]
 
 
@@ -39,6 +40,15 @@ class DQState(ctypes.Structure):
     """nf4_dq_state"""
     _fields_ = [("qabsmax", ctypes.c_void_p), ("code2", ctypes.c_void_p), ("absmax2", ctypes.c_void_p),
                 ("offset", ctypes.c_float), ("blocksize2", ctypes.c_int32)]
+
+
+class GemmWeight(ctypes.Structure):
+    """nf4_gemm_weight"""
+    _fields_ = [("packed", ctypes.c_void_p), ("absmax", ctypes.c_void_p), ("dq", DQState),
+                ("N", ctypes.c_int32), ("y", ctypes.c_void_p)]
+
+
+NF4_GEMM_MAX_GROUP = 4
 
 
 class TensorDesc(ctypes.Structure):
@@ -83,6 +93,8 @@ def load() -> ctypes.CDLL:
             "nf4_gemm": ([P, i32, i32, P, P, ctypes.POINTER(DQState), i32, i32, i32, P, i32, i32, P, i64, P], st),
             "nf4_gemm_default_splits": ([i32, i32, i32], i32),
             "nf4_gemm_workspace_bytes": ([i32, i32, i32, i32], i64),
+            "nf4_gemm_grouped": ([P, i32, i32, i32, i32, ctypes.POINTER(GemmWeight), i32, i32, P, i64, P], st),
+            "nf4_gemm_grouped_workspace_bytes": ([i32, ctypes.POINTER(ctypes.c_int32), i32, i32], i64),
             "nf4_dequantize_ex": ([P, P, ctypes.POINTER(DQState), i64, i32, P, i32, P, P], st),
             "nf4_dequantize_batched_ex": ([ctypes.POINTER(TensorDesc), i32, P, i32, P], st),
             "nf4_status_string": ([st], ctypes.c_char_p),
@@ -98,6 +110,8 @@ def load() -> ctypes.CDLL:
             "nf4_get_kernel_variant": ([], i32),
         }
         for name, (args, res) in sig.items():
+            if path != LIB_PATH and not hasattr(lib, name):
+                continue          # diagnostics build of an older revision (NF4_LIB): skip newer symbols
             fn = getattr(lib, name)
             fn.argtypes = args
             fn.restype = res

@@ -39,6 +39,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <type_traits>
 
@@ -53,24 +54,39 @@ constexpr int kCodeBytes = 32;              // packed bytes per row per k-chunk
 constexpr int kChunk = 64;          // k elements per stage (= one 128 B swizzle row in 16-bit)
 constexpr int kRowBytes = 128;
 
-struct GemmParams {
-  const uint8_t* packed;
+// One weight of a (grouped) GEMM: all members share X, K and the blocksize; their
+// output-feature tiles are concatenated into one tile stream.
+constexpr int kMaxMembers = 4;
+struct Member {
   const float* absmax;     // fp32 mode if non-null
   const uint8_t* qabsmax;  // DQ mode
   const float* code2;
   const float* absmax2;
-  const uint16_t* x;       // [M, K] 16-bit
-  void* y;                 // [M, N] (splits == 1)
-  float* partial;          // [splits, M, N] fp32 (splits > 1) / [parts, M, N] (stream-K)
-  unsigned* flags;         // stream-K: per-tile count of published partials (zero between calls)
+  void* y;                 // [M, N] row-major
   float offset;
-  int32_t M, N, K;
+  int32_t N;
+  int32_t tile0;           // first (global) 128-feature tile of this member
+};
+template <int NM>
+struct CodeMapsT {         // one TMA descriptor per member's packed codes
+  CUtensorMap m[NM];
+};
+using CodeMaps = CodeMapsT<kMaxMembers>;
+
+struct GemmParams {
+  Member mem[kMaxMembers];
+  int32_t nmem;
+  const uint16_t* x;       // [M, K] 16-bit
+  float* partial;          // [splits, M, Npad] fp32 (classic) / [parts, M, Npad] (stream-K)
+  unsigned* flags;         // stream-K: per-tile count of published partials (zero between calls)
+  int32_t M, K;
+  int32_t Npad;            // tiles_n * 128: row stride of the partials
   int32_t bs_shift;
   int32_t chunks_per_split;  // classic split-K
   int32_t splits;            // classic split-K (1 = direct output)
   int32_t out_dtype;         // NF4_F16 / NF4_BF16 / NF4_F32
   int32_t streamk;           // 1: stream-K ranges over a 1-D grid
-  int32_t tiles_n, tiles_m;  // tile grid (128 features x BN tokens)
+  int32_t tiles_n, tiles_m;  // tile grid (128 features x BN tokens), tiles_n over all members
   int32_t nk;                // 64-element chunks per tile (K / 64)
   int64_t total_chunks;      // tiles_n * tiles_m * nk
   int32_t align4;            // stream-K range bounds rounded to 4 chunks
@@ -202,9 +218,19 @@ __host__ __device__ __forceinline__ int64_t sk_owner(int64_t x, int64_t W, int64
   return c;
 }
 
+__device__ __forceinline__ int member_of(const GemmParams& p, int tn) {
+  int g = 0;
+#pragma unroll
+  for (int i = 1; i < kMaxMembers; ++i)
+    if (i < p.nmem && tn >= p.mem[i].tile0) g = i;
+  return g;
+}
+
 // One segment = a contiguous k-range of one output tile processed by one CTA.
 struct Segment {
-  int n0, m0;     // tile origin (features, tokens)
+  int g;          // member
+  int tn;         // global 128-feature tile index (partials, counters)
+  int n0, m0;     // tile origin (member-local features, tokens)
   int kc0, nk;    // first chunk within the tile, chunk count
   int part;       // partial-sum slot (stream-K: segment index within the tile; classic: split)
 };
@@ -241,11 +267,13 @@ struct SegIter {
   int phase;           // 0: head piece, 1: the rest
   int done_classic;
 };
-template <int BN>
+template <int BN, bool MULTI>
 __device__ __forceinline__ bool next_segment(const GemmParams& p, SegIter& it, Segment& sg) {
   if (!p.streamk) {
     if (it.done_classic) return false;
     it.done_classic = 1;
+    sg.g = 0;
+    sg.tn = blockIdx.x;
     sg.n0 = blockIdx.x * 128;
     sg.m0 = blockIdx.y * BN;
     sg.kc0 = blockIdx.z * p.chunks_per_split;
@@ -263,7 +291,9 @@ __device__ __forceinline__ bool next_segment(const GemmParams& p, SegIter& it, S
   const int tile = it.x / p.nk;
   const int tstart = tile * p.nk;
   const int send = min(it.end, tstart + p.nk);
-  sg.n0 = (tile % p.tiles_n) * 128;
+  sg.tn = tile % p.tiles_n;
+  sg.g = MULTI ? member_of(p, sg.tn) : 0;   // single weight: member 0 (constant-bank operands)
+  sg.n0 = (sg.tn - p.mem[sg.g].tile0) * 128;
   sg.m0 = (tile / p.tiles_n) * BN;
   sg.kc0 = it.x - tstart;
   sg.nk = send - it.x;
@@ -324,10 +354,11 @@ struct Scales {
 // holding the tile's last piece (its range's first segment) sums the partials
 // in piece order at the end of its range and writes y.  It waits only for
 // lower-numbered CTAs, dispatched before it.
-template <int BN, int G, int SUB, int CST, int NACC, bool BF16>
+template <int BN, int G, int SUB, int CST, int NACC, bool BF16, bool MULTI>
 __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
-    nf4_gemm_kernel(const __grid_constant__ GemmParams p, const __grid_constant__ CUtensorMap map_codes,
+    nf4_gemm_kernel(const __grid_constant__ GemmParams p, const __grid_constant__ CodeMapsT<MULTI ? kMaxMembers : 1> maps,
                     const __grid_constant__ CUtensorMap map_x) {
+  constexpr int kMem = MULTI ? kMaxMembers : 1;   // members this instantiation serves
   static_assert(CST >= G, "a super-stage slot must not be two phases behind any group");
   constexpr int kMmaWarp = 8 * G, kTmaWarp = 8 * G + 1;
   constexpr int ACC = BN < 32 ? 32 : BN;
@@ -337,7 +368,7 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
   constexpr int kSuperXBytes = SUB * BN * kRowBytes;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ __align__(256) float lut[16];                    // 256-B aligned: address = PRMT(offsets, base)
-  __shared__ float code2s[256];                               // DQ second-level table
+  __shared__ float code2s[kMem][256];                         // DQ second-level tables
   __shared__ __align__(8) uint64_t c_full[CST], c_free[CST], w_full[G], a_free[G], acc_full[NACC], acc_empty[NACC];
   __shared__ uint32_t tmem_holder;
   __shared__ int sk_range[3];                                 // stream-K: range start, end, first slot
@@ -384,7 +415,8 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   if (warp == kTmaWarp && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_codes)) : "memory");
+    for (int i = 0; i < kMem && i < p.nmem; ++i)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.m[i])) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_x)) : "memory");
   }
   // Programmatic dependent launch: the next kernel in the stream may start its own
@@ -392,8 +424,9 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
   // parameters and on-chip state, so it overlaps the previous kernel's tail.
   if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");   // inputs (and the workspace) are now ready
-  if (p.absmax == nullptr) {
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) code2s[i] = p.code2[i];
+  for (int i = 0; i < kMem && i < p.nmem; ++i) {
+    if (p.mem[i].absmax == nullptr)
+      for (int t = threadIdx.x; t < 256; t += blockDim.x) code2s[i][t] = p.mem[i].code2[t];
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -412,29 +445,37 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
     int J = 0, sidx = 0;                       // super-stages / segments before this segment
     SegIter it = seg_begin(p, sk_range);
     Segment sg;
-    while (next_segment<BN>(p, it, sg)) {
+    while (next_segment<BN, MULTI>(p, it, sg)) {
+      // this segment's weight (member of a grouped GEMM)
+      // (read from the parameter bank at each use: keeping them in registers spilled)
+#define absmax (p.mem[sg.g].absmax)
+#define qabsmax (p.mem[sg.g].qabsmax)
+#define absmax2 (p.mem[sg.g].absmax2)
+      const float offset = p.mem[sg.g].offset;
+      const float* c2 = code2s[sg.g];
+      const int Nm = p.mem[sg.g].N;
       const int row = sg.n0 + t;
-      const bool row_ok = row < p.N;
+      const bool row_ok = row < Nm;
       const int64_t blk_base = (int64_t(row) * p.K) >> p.bs_shift;
       const int nk = sg.nk, kc0 = sg.kc0;
       const int nsuper = (nk + SUB - 1) / SUB;
       const bool fast =
           SUB == 4 && p.bs_shift == 6 && (p.K % 256) == 0 && (kc0 % 4) == 0 &&
-          (p.absmax != nullptr ? (reinterpret_cast<uintptr_t>(p.absmax) & 15) == 0
-                               : (reinterpret_cast<uintptr_t>(p.qabsmax) & 3) == 0);
+          (absmax != nullptr ? (reinterpret_cast<uintptr_t>(absmax) & 15) == 0
+                               : (reinterpret_cast<uintptr_t>(qabsmax) & 3) == 0);
       auto fetch = [&](Scales& sc, int j) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) { sc.s[q] = 0; sc.a2[q] = 0.0f; }
         if (!row_ok) return;
         if (fast) {
           const int64_t b0 = blk_base + kc0 + 4 * j;
-          if (p.absmax != nullptr) {
-            const uint4 v = __ldg(reinterpret_cast<const uint4*>(p.absmax + b0));
+          if (absmax != nullptr) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(absmax + b0));
             sc.s[0] = v.x; sc.s[1] = v.y; sc.s[2] = v.z; sc.s[3] = v.w;
           } else {
-            sc.s[0] = __ldg(reinterpret_cast<const uint32_t*>(p.qabsmax + b0));
-            sc.a2[0] = __ldg(p.absmax2 + (b0 >> 8));
-            sc.a2[1] = __ldg(p.absmax2 + ((b0 + 3) >> 8));
+            sc.s[0] = __ldg(reinterpret_cast<const uint32_t*>(qabsmax + b0));
+            sc.a2[0] = __ldg(absmax2 + (b0 >> 8));
+            sc.a2[1] = __ldg(absmax2 + ((b0 + 3) >> 8));
           }
         } else {
 #pragma unroll
@@ -442,11 +483,11 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
             const int i = j * SUB + q;
             if (i < nk) {
               const int64_t b = blk_base + ((kc0 + i) >> chunk_shift);
-              if (p.absmax != nullptr) {
-                sc.s[q] = __float_as_uint(__ldg(p.absmax + b));
+              if (absmax != nullptr) {
+                sc.s[q] = __float_as_uint(__ldg(absmax + b));
               } else {
-                sc.s[q] = __ldg(p.qabsmax + b);
-                sc.a2[q] = __ldg(p.absmax2 + (b >> 8));
+                sc.s[q] = __ldg(qabsmax + b);
+                sc.a2[q] = __ldg(absmax2 + (b >> 8));
               }
             }
           }
@@ -485,9 +526,9 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
                 // A4 (R7): fl32(fl32(code2[qabsmax] * absmax2) + offset), two roundings
                 const uint32_t qb = (sc.s[0] >> (8 * q)) & 0xFFu;
                 const float a2 = ((b0 + q) >> 8) == (b0 >> 8) ? sc.a2[0] : sc.a2[1];
-                a = __fadd_rn(__fmul_rn(code2s[qb], a2), p.offset);
+                a = __fadd_rn(__fmul_rn(c2[qb], a2), offset);
               } else {
-                a = __fadd_rn(__fmul_rn(code2s[sc.s[q]], sc.a2[q]), p.offset);
+                a = __fadd_rn(__fmul_rn(c2[sc.s[q]], sc.a2[q]), offset);
               }
               const uint4 c0 = *reinterpret_cast<const uint4*>(smem_c + cs * kSuperCodeBytes +
                                                                code_chunk_off<SUB>(t, 2 * q + half));
@@ -526,7 +567,7 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
         using T_ = std::true_type;
         using F_ = std::false_type;
         const bool full = (j + 1) * SUB <= nk;
-        if (p.absmax != nullptr) {
+        if (absmax != nullptr) {
           if (full) stage(T_{}, std::integral_constant<int, 0>{}); else stage(F_{}, std::integral_constant<int, 0>{});
         } else if (fast) {
           if (full) stage(T_{}, std::integral_constant<int, 1>{}); else stage(F_{}, std::integral_constant<int, 1>{});
@@ -552,6 +593,7 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
         const int n = sg.n0 + qd * 32 + lane;
         const uint32_t taddr = tmem + (uint32_t(qd * 32) << 16) + uint32_t(ab * ACC);
         const bool direct = p.streamk ? (sg.kc0 == 0 && nk == p.nk) : p.splits == 1;
+        void* ym = p.mem[sg.g].y;
 #pragma unroll 1
         for (int cb = col0; cb < col0 + HB && cb < BN; cb += 16) {
           uint32_t v[16];
@@ -561,18 +603,18 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
                 "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
               : "r"(taddr + cb));
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          if (n < p.N) {
+          if (n < Nm) {
 #pragma unroll
             for (int jj = 0; jj < 16; ++jj) {
               const int m = sg.m0 + cb + jj;
               if (m < p.M) {
                 const float acc = nk > 0 ? __uint_as_float(v[jj]) : 0.0f;
                 if (!direct) {
-                  p.partial[(int64_t(sg.part) * p.M + m) * p.N + n] = acc;
+                  p.partial[(int64_t(sg.part) * p.M + m) * p.Npad + sg.tn * 128 + qd * 32 + lane] = acc;
                 } else if (p.out_dtype == NF4_F32) {
-                  static_cast<float*>(p.y)[int64_t(m) * p.N + n] = acc;
+                  static_cast<float*>(ym)[int64_t(m) * Nm + n] = acc;
                 } else {
-                  static_cast<uint16_t*>(p.y)[int64_t(m) * p.N + n] =
+                  static_cast<uint16_t*>(ym)[int64_t(m) * Nm + n] =
                       p.out_dtype == NF4_BF16 ? cvt1_rn<true>(acc) : cvt1_rn<false>(acc);
                 }
               }
@@ -586,20 +628,23 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
           // a non-final piece: publish (release) -- the tile's last CTA sums it at its end
           __threadfence();
           __syncwarp();
-          if (lane == 0) atomicAdd(p.flags + (sg.m0 / BN) * p.tiles_n + sg.n0 / 128, 1u);
+          if (lane == 0) atomicAdd(p.flags + (sg.m0 / BN) * p.tiles_n + sg.tn, 1u);
         }
         if (NF4_TRACING && threadIdx.x == 32 * 8 * g) p.trace[1024 + 4 * cta_lin + 3] = gtimer();
       }
       J += nsuper;
       ++sidx;
     }
+#undef absmax
+#undef qabsmax
+#undef absmax2
   } else if (warp == kTmaWarp) {
     // ======================= TMA issuer (one thread) =======================
     if (lane == 0) {
       int J = 0;
       SegIter it = seg_begin(p, sk_range);
       Segment sg;
-      while (next_segment<BN>(p, it, sg)) {
+      while (next_segment<BN, MULTI>(p, it, sg)) {
         const int nsuper = (sg.nk + SUB - 1) / SUB;
         for (int j = 0; j < nsuper; ++j) {
           const int Jg = J + j, cs = Jg % CST;
@@ -609,7 +654,7 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
           const bool ld_c = !(NF4_EXP(16)), ld_x = !(NF4_EXP(8));
           asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
               smem_u32(&c_full[cs])), "r"(uint32_t((ld_c ? kSuperCodeBytes : 0) + (ld_x ? kSuperXBytes : 0))) : "memory");
-          if (ld_c) tma_load_2d(smem_c + cs * kSuperCodeBytes, &map_codes, k0 / 2, sg.n0, &c_full[cs]);
+          if (ld_c) tma_load_2d(smem_c + cs * kSuperCodeBytes, &maps.m[sg.g], k0 / 2, sg.n0, &c_full[cs]);
           if (ld_x) {
 #pragma unroll
             for (int q = 0; q < SUB; ++q)
@@ -626,7 +671,7 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
     int J = 0, sidx = 0;
     SegIter it = seg_begin(p, sk_range);
     Segment sg;
-    while (next_segment<BN>(p, it, sg)) {
+    while (next_segment<BN, MULTI>(p, it, sg)) {
       const int nsuper = (sg.nk + SUB - 1) / SUB;
       const int ab = sidx % NACC;
       mbar_wait_parity(&acc_empty[ab], (uint32_t(sidx / NACC) & 1u) ^ 1u);   // its previous epilogue done
@@ -677,19 +722,23 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
         *flag = 0u;                                   // leave the workspace clean for the next call
       }
       __syncthreads();
-      const int n0 = (tile % p.tiles_n) * 128, m0 = (tile / p.tiles_n) * BN;
+      const int tn = tile % p.tiles_n, gm = MULTI ? member_of(p, tn) : 0;
+      const int n0 = (tn - p.mem[gm].tile0) * 128, m0 = (tile / p.tiles_n) * BN;
+      const int Nm = p.mem[gm].N;
+      void* ym = p.mem[gm].y;
       const int rows = min(BN, p.M - m0);
-      const int64_t mn = int64_t(p.M) * p.N;
+      const int64_t mn = int64_t(p.M) * p.Npad;
       for (int e = threadIdx.x; e < rows * 128; e += blockDim.x) {
         const int m = m0 + (e >> 7), n = n0 + (e & 127);
-        if (n >= p.N) continue;
-        const int64_t i = int64_t(m) * p.N + n;
+        if (n >= Nm) continue;
+        const int64_t i = int64_t(m) * p.Npad + tn * 128 + (e & 127);
         float acc = __ldcg(p.partial + i);
         for (int s2 = 1; s2 < parts; ++s2) acc = __fadd_rn(acc, __ldcg(p.partial + s2 * mn + i));
+        const int64_t o = int64_t(m) * Nm + n;
         if (p.out_dtype == NF4_F32)
-          static_cast<float*>(p.y)[i] = acc;
+          static_cast<float*>(ym)[o] = acc;
         else
-          static_cast<uint16_t*>(p.y)[i] = p.out_dtype == NF4_BF16 ? cvt1_rn<true>(acc) : cvt1_rn<false>(acc);
+          static_cast<uint16_t*>(ym)[o] = p.out_dtype == NF4_BF16 ? cvt1_rn<true>(acc) : cvt1_rn<false>(acc);
       }
     }
   }
@@ -702,11 +751,14 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
 
 // Deterministic reductions of the fp32 partials.
 // classic: y[m, n] = sum_s partial[s, m, n] in split order.
-__global__ void nf4_gemm_reduce_kernel(const float* __restrict__ partial, int splits, int64_t mn, void* y,
+// (classic split-K, one member; partial rows have stride Npad >= N)
+__global__ void nf4_gemm_reduce_kernel(const float* __restrict__ partial, int splits, int M, int N, int Npad, void* y,
                                        int out_dtype) {
+  const int64_t mn = int64_t(M) * N, mnp = int64_t(M) * Npad;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < mn; i += int64_t(gridDim.x) * blockDim.x) {
-    float acc = partial[i];
-    for (int s = 1; s < splits; ++s) acc = __fadd_rn(acc, partial[int64_t(s) * mn + i]);
+    const int64_t j = (i / N) * Npad + i % N;
+    float acc = partial[j];
+    for (int s = 1; s < splits; ++s) acc = __fadd_rn(acc, partial[int64_t(s) * mnp + j]);
     if (out_dtype == NF4_F32)
       static_cast<float*>(y)[i] = acc;
     else
@@ -731,15 +783,17 @@ constexpr size_t smem_bytes() {
   return 1024 /*align slack*/ + size_t(cst_for<BN>()) * sub_for<BN>() * (128 * kCodeBytes + BN * kRowBytes);
 }
 
-template <int BN, bool BF16>
+template <int BN, bool BF16, bool MULTI>
 constexpr auto kernel_for() {
-  return nf4_gemm_kernel<BN, kGroups, sub_for<BN>(), cst_for<BN>(), nacc_for<BN>(), BF16>;
+  return nf4_gemm_kernel<BN, kGroups, sub_for<BN>(), cst_for<BN>(), nacc_for<BN>(), BF16, MULTI>;
 }
 
-template <int BN, bool BF16>
-static cudaError_t launch(const GemmParams& p, const CUtensorMap& mc, const CUtensorMap& mx, dim3 grid,
-                          cudaStream_t s) {
-  auto k = kernel_for<BN, BF16>();
+template <int BN, bool BF16, bool MULTI>
+static cudaError_t launch1(const GemmParams& p, const CodeMaps& mc, const CUtensorMap& mx, dim3 grid,
+                           cudaStream_t s) {
+  auto k = kernel_for<BN, BF16, MULTI>();
+  CodeMapsT<MULTI ? kMaxMembers : 1> maps;
+  memcpy(&maps, &mc, sizeof(maps));
   constexpr size_t sm = smem_bytes<BN>();
   static std::once_flag once;          // per instantiation (per process: one device type)
   static cudaError_t attr = cudaSuccess;
@@ -757,9 +811,15 @@ static cudaError_t launch(const GemmParams& p, const CUtensorMap& mc, const CUte
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, k, p, mc, mx);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, k, p, maps, mx);
   if (e != cudaSuccess) return e;
   return cudaPeekAtLastError();
+}
+
+template <int BN, bool BF16>
+static cudaError_t launch(const GemmParams& p, const CodeMaps& mc, const CUtensorMap& mx, dim3 grid,
+                          cudaStream_t s) {
+  return p.nmem > 1 ? launch1<BN, BF16, true>(p, mc, mx, grid, s) : launch1<BN, BF16, false>(p, mc, mx, grid, s);
 }
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -866,16 +926,37 @@ static int64_t sk_flag_bytes(const SkGeom& g) {
   return (int64_t(g.tiles_n) * g.tiles_m * 4 + 255) / 256 * 256;
 }
 
+static int64_t npad_of(int32_t N) { return int64_t((N + 127) / 128) * 128; }
+
+// Stream-K workspace for an [M, K] x [Npad, K]^T problem, -1 when the chunk
+// stream exceeds the kernel's 32-bit indices (the caller then needs the classic grid).
+static int64_t streamk_ws_bytes(int32_t M, int64_t Npad, int32_t K) {
+  const SkGeom g = sk_geometry(M, int32_t(Npad), K);
+  if (g.W >= (int64_t(1) << 31)) return -1;
+  return g.max_parts > 1 ? sk_flag_bytes(g) + int64_t(g.max_parts) * M * Npad * 4 : 0;
+}
+
 extern "C" int64_t nf4_gemm_workspace_bytes(int32_t M, int32_t N, int32_t K, int32_t splits) {
   if (M <= 0 || N <= 0 || K <= 0) return 0;
   if (splits <= 0) {
     if (K % 64 != 0) return 0;
-    const SkGeom g = sk_geometry(M, N, K);
-    if (g.W >= (int64_t(1) << 31)) return nf4_gemm_workspace_bytes(M, N, K, nf4_gemm_default_splits(M, N, K));
-    return g.max_parts > 1 ? sk_flag_bytes(g) + int64_t(g.max_parts) * M * N * 4 : 0;
+    const int64_t b = streamk_ws_bytes(M, npad_of(N), K);
+    if (b >= 0) return b;
+    splits = nf4_gemm_default_splits(M, N, K);   // classic fallback (nf4_gemm does the same)
   }
   if (splits <= 1) return 0;
-  return int64_t(splits) * M * N * 4;
+  return int64_t(splits) * M * npad_of(N) * 4;
+}
+
+extern "C" int64_t nf4_gemm_grouped_workspace_bytes(int32_t M, const int32_t* N, int32_t count, int32_t K) {
+  if (M <= 0 || K <= 0 || K % 64 != 0 || !N || count <= 0 || count > kMaxMembers) return 0;
+  int64_t npad = 0;
+  for (int i = 0; i < count; ++i) {
+    if (N[i] <= 0) return 0;
+    npad += npad_of(N[i]);
+  }
+  const int64_t b = streamk_ws_bytes(M, npad, K);
+  return b > 0 ? b : 0;
 }
 
 // Split-K factor minimising the makespan of the (row tile, token tile, split)
@@ -900,34 +981,64 @@ extern "C" int32_t nf4_gemm_default_splits(int32_t M, int32_t N, int32_t K) {
   return best_s;
 }
 
-extern "C" nf4_status nf4_gemm(const void* x, nf4_dtype x_dtype, int32_t M, const uint8_t* packed,
-                               const float* absmax, const nf4_dq_state* dq, int32_t N, int32_t K, int32_t blocksize,
-                               void* y, nf4_dtype y_dtype, int32_t splits, void* workspace,
-                               int64_t workspace_bytes, void* stream) {
-  if (M < 0 || N < 0 || K < 0) return NF4_ERR_BAD_SIZE;
+// One weight as the host sees it (nf4_gemm: one; nf4_gemm_grouped: up to 4).
+struct HostMember {
+  const uint8_t* packed;
+  const float* absmax;
+  const nf4_dq_state* dq;
+  int32_t N;
+  void* y;
+};
+
+static nf4_status check_member(const HostMember& m, nf4_dtype y_dtype) {
+  if (m.N < 0) return NF4_ERR_BAD_SIZE;
+  if ((m.absmax == nullptr) == (m.dq == nullptr)) return NF4_ERR_BAD_STATE;
+  if (m.dq && m.dq->blocksize2 != 256) return NF4_ERR_BAD_STATE;
+  if (m.N == 0) return NF4_OK;
+  if (!m.packed || !m.y) return NF4_ERR_NULL_POINTER;
+  if (m.dq && (!m.dq->qabsmax || !m.dq->code2 || !m.dq->absmax2)) return NF4_ERR_NULL_POINTER;
+  if (!aligned(m.packed, 16)) return NF4_ERR_MISALIGNED;
+  if (!aligned(m.y, y_dtype == NF4_F32 ? 4 : 2)) return NF4_ERR_MISALIGNED;
+  if (m.absmax && !aligned(m.absmax, 4)) return NF4_ERR_MISALIGNED;
+  return NF4_OK;
+}
+
+static nf4_status gemm_run(const void* x, nf4_dtype x_dtype, int32_t M, int32_t K, int32_t blocksize,
+                           const HostMember* mem_in, int32_t count, nf4_dtype y_dtype, int32_t splits, void* workspace,
+                           int64_t workspace_bytes, void* stream) {
+  if (M < 0 || K < 0 || count < 1 || count > kMaxMembers) return NF4_ERR_BAD_SIZE;
   if (x_dtype != NF4_F16 && x_dtype != NF4_BF16) return NF4_ERR_BAD_DTYPE;
   if (y_dtype != NF4_F16 && y_dtype != NF4_BF16 && y_dtype != NF4_F32) return NF4_ERR_BAD_DTYPE;
   if (!is_pow2(blocksize) || blocksize < 64 || blocksize > 4096) return NF4_ERR_BAD_BLOCKSIZE;
-  if ((absmax == nullptr) == (dq == nullptr)) return NF4_ERR_BAD_STATE;
-  if (dq && dq->blocksize2 != 256) return NF4_ERR_BAD_STATE;
-  if (M == 0 || N == 0) { set_launch_count(0); return NF4_OK; }
+  for (int i = 0; i < count; ++i) {
+    const nf4_status st = check_member(mem_in[i], y_dtype);
+    if (st != NF4_OK) return st;
+  }
+  // members with N == 0 contribute no tiles
+  HostMember mem[kMaxMembers];
+  int nmem = 0;
+  for (int i = 0; i < count; ++i)
+    if (mem_in[i].N > 0) mem[nmem++] = mem_in[i];
+  if (M == 0 || nmem == 0) { set_launch_count(0); return NF4_OK; }
   if (K % 64 != 0 || K % blocksize != 0) return NF4_ERR_BAD_SIZE;  // a 64-chunk never spans two blocks
-  if (!x || !packed || !y) return NF4_ERR_NULL_POINTER;
-  if (dq && (!dq->qabsmax || !dq->code2 || !dq->absmax2)) return NF4_ERR_NULL_POINTER;
-  if (!aligned(x, 16) || !aligned(packed, 16)) return NF4_ERR_MISALIGNED;
-  if (!aligned(y, y_dtype == NF4_F32 ? 4 : 2)) return NF4_ERR_MISALIGNED;
-  if (absmax && !aligned(absmax, 4)) return NF4_ERR_MISALIGNED;
+  if (!x) return NF4_ERR_NULL_POINTER;
+  if (!aligned(x, 16)) return NF4_ERR_MISALIGNED;
   const int nk = K / 64;
-  // stream-K chunk indices are 32-bit in the kernel; beyond that, the classic grid
-  const int64_t w_chunks = int64_t((N + 127) / 128) * ((M + pick_bn(M) - 1) / pick_bn(M)) * nk;
-  const bool streamk = splits <= 0 && nk > 0 && w_chunks < (int64_t(1) << 31);
-  if (splits <= 0 && !streamk) splits = nf4_gemm_default_splits(M, N, K);
+  const int bn = pick_bn(M);
+  int tiles_n = 0;
+  for (int i = 0; i < nmem; ++i) tiles_n += (mem[i].N + 127) / 128;
+  const int64_t npad = int64_t(tiles_n) * 128;
+  // stream-K chunk indices are 32-bit in the kernel; beyond that, the classic grid (one weight only)
+  const int64_t w_chunks = int64_t(tiles_n) * ((M + bn - 1) / bn) * nk;
+  const bool streamk = (splits <= 0 || nmem > 1) && nk > 0 && w_chunks < (int64_t(1) << 31);
+  if (!streamk && nmem > 1) return NF4_ERR_BAD_SIZE;
+  if (splits <= 0 && !streamk) splits = nf4_gemm_default_splits(M, mem[0].N, K);
   SkGeom g{};
   if (streamk) {
-    g = sk_geometry(M, N, K);
+    g = sk_geometry(M, int32_t(npad), K);
     if (g.max_parts > 1) {
       if (!workspace) return NF4_ERR_NULL_POINTER;
-      if (workspace_bytes < sk_flag_bytes(g) + int64_t(g.max_parts) * M * N * 4) return NF4_ERR_BAD_STATE;
+      if (workspace_bytes < sk_flag_bytes(g) + int64_t(g.max_parts) * M * npad * 4) return NF4_ERR_BAD_STATE;
       if (!aligned(workspace, 16)) return NF4_ERR_MISALIGNED;
     }
     splits = 1;
@@ -936,19 +1047,31 @@ extern "C" nf4_status nf4_gemm(const void* x, nf4_dtype x_dtype, int32_t M, cons
     if (splits > nk) splits = nk > 0 ? nk : 1;
     if (splits > 1) {
       if (!workspace) return NF4_ERR_NULL_POINTER;
-      if (workspace_bytes < nf4_gemm_workspace_bytes(M, N, K, splits)) return NF4_ERR_BAD_STATE;
+      if (workspace_bytes < int64_t(splits) * M * npad * 4) return NF4_ERR_BAD_STATE;
       if (!aligned(workspace, 16)) return NF4_ERR_MISALIGNED;
     }
   }
   GemmParams p;
-  p.packed = packed;
-  p.absmax = absmax;
-  p.qabsmax = dq ? dq->qabsmax : nullptr;
-  p.code2 = dq ? dq->code2 : nullptr;
-  p.absmax2 = dq ? dq->absmax2 : nullptr;
-  p.offset = dq ? dq->offset : 0.0f;
+  int tile0 = 0;
+  for (int i = 0; i < kMaxMembers; ++i) {
+    Member& m = p.mem[i];
+    if (i < nmem) {
+      m.absmax = mem[i].absmax;
+      m.qabsmax = mem[i].dq ? mem[i].dq->qabsmax : nullptr;
+      m.code2 = mem[i].dq ? mem[i].dq->code2 : nullptr;
+      m.absmax2 = mem[i].dq ? mem[i].dq->absmax2 : nullptr;
+      m.offset = mem[i].dq ? mem[i].dq->offset : 0.0f;
+      m.N = mem[i].N;
+      m.y = mem[i].y;
+      m.tile0 = tile0;
+      tile0 += (mem[i].N + 127) / 128;
+    } else {
+      m = Member{};
+      m.tile0 = 1 << 30;
+    }
+  }
+  p.nmem = nmem;
   p.x = static_cast<const uint16_t*>(x);
-  p.y = y;
   p.partial = static_cast<float*>(workspace);
   p.flags = nullptr;
   if (streamk && g.max_parts > 1) {
@@ -956,13 +1079,12 @@ extern "C" nf4_status nf4_gemm(const void* x, nf4_dtype x_dtype, int32_t M, cons
     p.partial = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + sk_flag_bytes(g));
   }
   p.M = M;
-  p.N = N;
   p.K = K;
+  p.Npad = int32_t(npad);
   p.bs_shift = log2i(blocksize);
+  const int sub = bn <= 64 ? 4 : bn <= 128 ? 2 : 1;
   {
     // whole super-stages per split (SUB chunks share one TMA box); splits = non-empty ranges
-    const int bn0 = pick_bn(M);
-    const int sub = bn0 <= 64 ? 4 : bn0 <= 128 ? 2 : 1;
     int cps = (nk + splits - 1) / splits;
     cps = (cps + sub - 1) / sub * sub;
     splits = (nk + cps - 1) / cps;
@@ -971,8 +1093,8 @@ extern "C" nf4_status nf4_gemm(const void* x, nf4_dtype x_dtype, int32_t M, cons
   p.splits = splits;
   p.out_dtype = int(y_dtype);
   p.streamk = streamk ? 1 : 0;
-  p.tiles_n = (N + 127) / 128;
-  p.tiles_m = (M + pick_bn(M) - 1) / pick_bn(M);
+  p.tiles_n = tiles_n;
+  p.tiles_m = (M + bn - 1) / bn;
   p.nk = nk;
   p.total_chunks = int64_t(p.tiles_n) * p.tiles_m * nk;
   p.align4 = streamk ? g.align4 : 0;
@@ -983,17 +1105,19 @@ extern "C" nf4_status nf4_gemm(const void* x, nf4_dtype x_dtype, int32_t M, cons
   if (const char* ex = getenv("NF4_GEMM_EXPERIMENT")) p.experiment = atoi(ex);
 #endif
   nf4_codebook(p.lut);
-  const int bn = pick_bn(M);
-  dim3 grid = streamk ? dim3(unsigned(g.G), 1, 1) : dim3((N + 127) / 128, (M + bn - 1) / bn, splits);
+  dim3 grid = streamk ? dim3(unsigned(g.G), 1, 1) : dim3(unsigned(tiles_n), unsigned(p.tiles_m), unsigned(splits));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool bf16 = x_dtype == NF4_BF16;
-  CUtensorMap mc, mx;
-  const int sub = bn <= 64 ? 4 : bn <= 128 ? 2 : 1;
+  CodeMaps mc;
+  memset(&mc, 0, sizeof(mc));
+  CUtensorMap mx;
   const CUtensorMapSwizzle csw = sub == 4 ? CU_TENSOR_MAP_SWIZZLE_128B
                                  : sub == 2 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
-  if (!make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, packed, uint64_t(K) / 2, uint64_t(N), uint32_t(sub * kCodeBytes),
-                128, csw) ||
-      !make_map(&mx, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, x, uint64_t(K),
+  for (int i = 0; i < nmem; ++i)
+    if (!make_map(&mc.m[i], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, mem[i].packed, uint64_t(K) / 2, uint64_t(mem[i].N),
+                  uint32_t(sub * kCodeBytes), 128, csw))
+      return NF4_ERR_CUDA;
+  if (!make_map(&mx, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, x, uint64_t(K),
                 uint64_t(M), kChunk, uint32_t(bn), CU_TENSOR_MAP_SWIZZLE_128B))
     return NF4_ERR_CUDA;
   cudaError_t e;
@@ -1007,13 +1131,36 @@ extern "C" nf4_status nf4_gemm(const void* x, nf4_dtype x_dtype, int32_t M, cons
   if (e != cudaSuccess) { cudaGetLastError(); return NF4_ERR_CUDA; }
   int launches = 1;
   if (!streamk && splits > 1) {
-    const int64_t mn = int64_t(M) * N;
-    int64_t g = (mn + 255) / 256;
-    if (g > int64_t(sm_count()) * 8) g = int64_t(sm_count()) * 8;
-    nf4_gemm_reduce_kernel<<<int(g), 256, 0, s>>>(static_cast<const float*>(workspace), splits, mn, y, int(y_dtype));
+    const int64_t mn = int64_t(M) * mem[0].N;
+    int64_t gr = (mn + 255) / 256;
+    if (gr > int64_t(sm_count()) * 8) gr = int64_t(sm_count()) * 8;
+    nf4_gemm_reduce_kernel<<<int(gr), 256, 0, s>>>(static_cast<const float*>(workspace), splits, M, mem[0].N,
+                                                   int(npad), mem[0].y, int(y_dtype));
     if (cudaPeekAtLastError() != cudaSuccess) { cudaGetLastError(); return NF4_ERR_CUDA; }
     ++launches;
   }
   set_launch_count(launches);
   return NF4_OK;
+}
+
+extern "C" nf4_status nf4_gemm(const void* x, nf4_dtype x_dtype, int32_t M, const uint8_t* packed,
+                               const float* absmax, const nf4_dq_state* dq, int32_t N, int32_t K, int32_t blocksize,
+                               void* y, nf4_dtype y_dtype, int32_t splits, void* workspace,
+                               int64_t workspace_bytes, void* stream) {
+  if (N < 0) return NF4_ERR_BAD_SIZE;
+  const HostMember m{packed, absmax, dq, N, y};
+  return gemm_run(x, x_dtype, M, K, blocksize, &m, 1, y_dtype, splits, workspace, workspace_bytes, stream);
+}
+
+extern "C" nf4_status nf4_gemm_grouped(const void* x, nf4_dtype x_dtype, int32_t M, int32_t K, int32_t blocksize,
+                                       const nf4_gemm_weight* weights, int32_t count, nf4_dtype y_dtype,
+                                       void* workspace, int64_t workspace_bytes, void* stream) {
+  if (count < 1 || count > NF4_GEMM_MAX_GROUP) return NF4_ERR_BAD_SIZE;
+  if (!weights) return NF4_ERR_NULL_POINTER;
+  HostMember m[kMaxMembers];
+  for (int i = 0; i < count; ++i) {
+    const nf4_gemm_weight& w = weights[i];
+    m[i] = HostMember{w.packed, w.absmax, w.absmax ? nullptr : &w.dq, w.N, w.y};
+  }
+  return gemm_run(x, x_dtype, M, K, blocksize, m, count, y_dtype, 0, workspace, workspace_bytes, stream);
 }

@@ -109,3 +109,46 @@ class NF4Linear(torch.nn.Module):
     def extra_repr(self) -> str:
         return (f"in_features={self.in_features}, out_features={self.out_features}, blocksize={self.blocksize}, "
                 f"double_quant={self.double_quant}, compute_dtype={self.compute_dtype}")
+
+
+class NF4LinearGroup(torch.nn.Module):
+    """Up to 4 NF4Linear layers that consume the same input (q/k/v, gate/up): one
+    ``nf4_gemm_grouped`` launch for decode-size inputs, so the fused kernel's
+    fill/drain is paid once per group.  Larger M falls back to the
+    members' own forward.  Returns a list with one output per member."""
+
+    def __init__(self, members):
+        super().__init__()
+        members = list(members)
+        if not 1 <= len(members) <= 4:
+            raise ValueError("1..4 members")
+        k = members[0].in_features
+        if any(m.in_features != k or m.blocksize != members[0].blocksize or
+               m.compute_dtype != members[0].compute_dtype for m in members):
+            raise ValueError("members must share in_features, blocksize and compute_dtype")
+        self.members = torch.nn.ModuleList(members)
+        self._ws: dict = {}
+
+    def forward(self, x: torch.Tensor):
+        from . import nf4_gemm_grouped, nf4_gemm_grouped_workspace_bytes
+        m0 = self.members[0]
+        shape = x.shape
+        x2 = x.reshape(-1, m0.in_features).to(m0.compute_dtype).contiguous()
+        M, K = x2.shape
+        fused_ok = (M <= m0.fused_max_m and K % 64 == 0 and K % m0.blocksize == 0 and x2.data_ptr() % 16 == 0
+                    and all(m.packed.data_ptr() % 16 == 0 for m in self.members))
+        if not fused_ok:
+            return [m(x) for m in self.members]
+        Ns = tuple(m.out_features for m in self.members)
+        ws = self._ws.get(M)
+        if ws is None:
+            nbytes = nf4_gemm_grouped_workspace_bytes(M, Ns, K)
+            ws = self._ws[M] = torch.zeros(max(nbytes, 16), dtype=torch.uint8, device=x.device)
+        weights = [(m.packed, m.absmax, m._dq(), m.out_features) for m in self.members]
+        ys = nf4_gemm_grouped(x2, weights, K=K, blocksize=m0.blocksize, y_dtype=m0.compute_dtype, workspace=ws)
+        out = []
+        for m, y in zip(self.members, ys):
+            if m.bias is not None:
+                y = y + m.bias
+            out.append(y.reshape(*shape[:-1], m.out_features))
+        return out

@@ -200,6 +200,74 @@ def test_gemm_stream_k_workspace_reuse(nf4, orc):
         assert int(ws[:4 * tiles].view(torch.int32).abs().sum()) == 0, "stream-K counters not reset"
 
 
+@pytest.mark.parametrize("M", [5, 16, 40])
+def test_gemm_grouped_bit_exact_weights_and_bound(nf4, orc, M):
+    """nf4_gemm_grouped: q/k/v-like members (different N, one not a multiple of 128,
+    fp32 and double-quant absmax) in one launch; one-hot X checks every member's
+    weights bit-exactly, random X against the fp64 oracle bound."""
+    import torch
+    K = 1536
+    Ns = (1024, 200, 384)
+    dqs = (True, False, True)
+    members, kws, packs = [], [], []
+    for i, (N, dq) in enumerate(zip(Ns, dqs)):
+        packed, kw = _weights(N, K, 64, dq, seed=300 + i)
+        packs.append(packed)
+        kws.append(kw)
+        if dq:
+            d = nf4.DQ(dev(kw["qabsmax"]), dev(kw["code2"]), dev(kw["absmax2"]), kw["offset"])
+            members.append((dev(packed), None, d, N))
+        else:
+            members.append((dev(packed), dev(kw["absmax"]), None, N))
+    # one-hot rows: Y_i[m, n] = W_i[n, k_m] exactly
+    ks = (np.arange(M) * 131 + 7) % K
+    xo = np.zeros((M, K), np.float32)
+    xo[np.arange(M), ks] = 1.0
+    x16 = xo.astype(ml_dtypes.bfloat16).view(np.uint16)
+    x = dev(x16.view(np.int16)).view(torch.bfloat16).reshape(M, K)
+    ys = nf4.nf4_gemm_grouped(x, members, K=K, y_dtype="f32")
+    torch.cuda.synchronize()
+    for i, N in enumerate(Ns):
+        w16 = orc.dequantize(packs[i], N * K, 64, orc.OUT_BF16, threads=8, **kws[i]).reshape(N, K)
+        want = w16[:, ks].T.view(ml_dtypes.bfloat16).astype(np.float32)
+        assert np.array_equal(ys[i].cpu().numpy().view(np.uint32), want.view(np.uint32)), (M, i)
+    # random X, within the fp32 accumulation bound
+    rng = np.random.Generator(np.random.Philox(M))
+    x16 = rng.standard_normal((M, K)).astype(np.float32).astype(ml_dtypes.bfloat16).view(np.uint16)
+    x = dev(x16.view(np.int16)).view(torch.bfloat16).reshape(M, K)
+    ys = nf4.nf4_gemm_grouped(x, members, K=K, y_dtype="f32")
+    torch.cuda.synchronize()
+    for i, N in enumerate(Ns):
+        ref, mag = orc.gemm_reference(x16, orc.OUT_BF16, packs[i], N, K, 64, **kws[i])
+        err = np.abs(ys[i].cpu().numpy().astype(np.float64) - ref)
+        assert (err <= K * 2.0 ** -23 * mag + 1e-30).all(), (M, i)
+
+
+def test_gemm_grouped_workspace_reuse_and_errors(nf4, orc):
+    import torch
+    M, K = 16, 2048
+    Ns = (2048, 512)
+    members, kws, packs = [], [], []
+    for i, N in enumerate(Ns):
+        packed, kw = _weights(N, K, 64, False, seed=400 + i)
+        packs.append(packed)
+        kws.append(kw)
+        members.append((dev(packed), dev(kw["absmax"]), None, N))
+    ws = torch.zeros(max(16, nf4.nf4_gemm_grouped_workspace_bytes(M, Ns, K)), dtype=torch.uint8, device="cuda")
+    rng = np.random.Generator(np.random.Philox(4))
+    for rep in range(3):
+        x16 = rng.standard_normal((M, K)).astype(np.float32).astype(ml_dtypes.bfloat16).view(np.uint16)
+        x = dev(x16.view(np.int16)).view(torch.bfloat16).reshape(M, K)
+        ys = nf4.nf4_gemm_grouped(x, members, K=K, y_dtype="f32", workspace=ws)
+        torch.cuda.synchronize()
+        for i, N in enumerate(Ns):
+            ref, mag = orc.gemm_reference(x16, orc.OUT_BF16, packs[i], N, K, 64, **kws[i])
+            assert (np.abs(ys[i].cpu().numpy().astype(np.float64) - ref) <= K * 2.0 ** -23 * mag + 1e-30).all()
+    with pytest.raises(nf4.NF4Error) as e:
+        nf4.nf4_gemm_grouped(x, members * 3, K=K)             # 6 weights > NF4_GEMM_MAX_GROUP
+    assert e.value.status == 2
+
+
 def test_gemm_argument_errors(nf4):
     import torch
     x = torch.zeros((4, 100), dtype=torch.bfloat16, device="cuda")

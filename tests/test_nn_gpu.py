@@ -54,3 +54,24 @@ def test_nf4linear_matches_oracle(nn, orc, dq):
         ref, mag = xd @ wd.T, np.abs(xd) @ np.abs(wd).T
         bound = in_f * 2.0 ** -23 * mag * (1 + 2.0 ** -8) + np.abs(ref) * 2.0 ** -8 + 1e-30
         assert (np.abs(y - ref) <= bound).all(), M
+
+
+def test_nf4lineargroup_matches_members(nn):
+    """NF4LinearGroup (one grouped launch) agrees with each member's own forward
+    within the fp32 accumulation bound, and falls back for prefill-size M."""
+    import torch
+    in_f = 1024
+    lins = []
+    for i, out_f in enumerate((512, 256, 256)):
+        w = syn.gaussian_weights(out_f * in_f, 20 + i).reshape(out_f, in_f)
+        lins.append(nn.NF4Linear.from_weight(torch.from_numpy(w).cuda(), double_quant=(i != 1)))
+    grp = nn.NF4LinearGroup(lins)
+    for M in (1, 16, 300):
+        x = torch.from_numpy(syn.gaussian_weights(M * in_f, 7 + M, std=1.0).reshape(M, in_f)).cuda().to(torch.bfloat16)
+        outs = grp(x)
+        for lin, y in zip(lins, outs):
+            wd = lin.dequantize().float().double()
+            xd = x.double()
+            ref, mag = xd @ wd.T, xd.abs() @ wd.abs().T
+            bound = in_f * 2.0 ** -23 * mag * (1 + 2.0 ** -8) + ref.abs() * 2.0 ** -8 + 1e-30
+            assert ((y.double() - ref).abs() <= bound).all(), M

@@ -39,6 +39,8 @@ def main():
     ap.add_argument("--splits", type=int, default=0,
                     help="0: stream-K (default); -1: classic grid, makespan split heuristic; >0: classic, fixed")
     ap.add_argument("--no-unfused", action="store_true")
+    ap.add_argument("--grouped", action="store_true",
+                    help="q/k/v and gate/up of each layer as one nf4_gemm_grouped launch (they share X)")
     args = ap.parse_args()
 
     torch.cuda.set_device(0)
@@ -84,7 +86,41 @@ def main():
         torch.cuda.synchronize()
         return a.elapsed_time(b) / args.steps
 
-    fused_ms = timeit(fused_step)
+    # groups of consecutive weights sharing X: (q, k, v), (o), (gate, up), (down) per layer
+    groups = []
+    cur = []
+    for i, t in enumerate(tensors):
+        kind = t.name.split(".")[2].split("[")[0]
+        key = {"q_proj": "qkv", "k_proj": "qkv", "v_proj": "qkv", "gate_proj": "gu", "up_proj": "gu"}.get(kind, kind)
+        lay = t.name.split(".")[1]
+        if cur and (cur[0][1] != (lay, key) or key not in ("qkv", "gu")):
+            groups.append([c[0] for c in cur])
+            cur = []
+        cur.append((i, (lay, key)))
+    if cur:
+        groups.append([c[0] for c in cur])
+    gws = {}
+    for grp in groups:
+        if len(grp) > 1:
+            Ns = tuple(tensors[i].rows for i in grp)
+            K = tensors[grp[0]].cols
+            gws[tuple(grp)] = torch.zeros(max(16, nf4.nf4_gemm_grouped_workspace_bytes(M, Ns, K)),
+                                          dtype=torch.uint8, device="cuda")
+
+    def grouped_step():
+        for grp in groups:
+            if len(grp) == 1:
+                i = grp[0]
+                t, e = tensors[i], ws.entries[i]
+                key = (t.rows, t.cols)
+                nf4.nf4_gemm(xs[t.cols], ws._ptr(ws.codes, e.codes_off), None, dqs[i], N=t.rows, K=t.cols,
+                             y=ys[i], splits=splits[key], workspace=wsp[key])
+            else:
+                K = tensors[grp[0]].cols
+                members = [(ws._ptr(ws.codes, ws.entries[i].codes_off), None, dqs[i], tensors[i].rows) for i in grp]
+                nf4.nf4_gemm_grouped(xs[K], members, K=K, ys=[ys[i] for i in grp], workspace=gws[tuple(grp)])
+
+    fused_ms = timeit(grouped_step if args.grouped else fused_step)
     n_total = sum(t.n for t in tensors)
     bytes_w = sum((e.n // 2) + (e.n // 64) + 4 * (e.n // 64 // 256) for e in ws.entries)
     bytes_xy = sum(M * t.cols * 2 + M * t.rows * 2 for t in tensors)
@@ -94,7 +130,8 @@ def main():
            "fused_ms": round(fused_ms, 4),
            "fused_hbm_gbs": round((bytes_w + bytes_xy) / (fused_ms * 1e-3) / 1e9, 1),
            "fused_tflops": round(flops / (fused_ms * 1e-3) / 1e12, 2),
-           "splits": sorted(set(splits.values()))}
+           "splits": sorted(set(splits.values())), "grouped": bool(args.grouped),
+           "launches_per_step": len(groups) if args.grouped else len(tensors)}
     if not args.no_unfused:
         wbuf = torch.empty(max(t.n for t in tensors), dtype=torch.bfloat16, device="cuda")
 
