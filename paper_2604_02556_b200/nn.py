@@ -117,8 +117,9 @@ class NF4LinearGroup(torch.nn.Module):
     fill/drain is paid once per group.  Larger M falls back to the
     members' own forward.  Returns a list with one output per member."""
 
-    def __init__(self, members):
+    def __init__(self, members, fused_max_m: int = 256):
         super().__init__()
+        self.fused_max_m = fused_max_m   # grouped fused beats dequantize+cuBLAS up to M = 256 (r01)
         members = list(members)
         if not 1 <= len(members) <= 4:
             raise ValueError("1..4 members")
@@ -135,7 +136,7 @@ class NF4LinearGroup(torch.nn.Module):
         shape = x.shape
         x2 = x.reshape(-1, m0.in_features).to(m0.compute_dtype).contiguous()
         M, K = x2.shape
-        fused_ok = (M <= m0.fused_max_m and K % 64 == 0 and K % m0.blocksize == 0 and x2.data_ptr() % 16 == 0
+        fused_ok = (M <= self.fused_max_m and K % 64 == 0 and K % m0.blocksize == 0 and x2.data_ptr() % 16 == 0
                     and all(m.packed.data_ptr() % 16 == 0 for m in self.members))
         if not fused_ok:
             return [m(x) for m in self.members]

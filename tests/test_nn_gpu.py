@@ -66,7 +66,7 @@ def test_nf4lineargroup_matches_members(nn):
         w = syn.gaussian_weights(out_f * in_f, 20 + i).reshape(out_f, in_f)
         lins.append(nn.NF4Linear.from_weight(torch.from_numpy(w).cuda(), double_quant=(i != 1)))
     grp = nn.NF4LinearGroup(lins)
-    for M in (1, 16, 300):
+    for M in (1, 16, 200, 300):
         x = torch.from_numpy(syn.gaussian_weights(M * in_f, 7 + M, std=1.0).reshape(M, in_f)).cuda().to(torch.bfloat16)
         outs = grp(x)
         for lin, y in zip(lins, outs):
