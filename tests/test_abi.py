@@ -111,6 +111,27 @@ def test_argument_validation_without_gpu(lib):
     assert lib.nf4_dequantize_host(fake, fake, None, 1 << 20, 64, 0, fake, P(0x10000), 1 << 30, 1000, None) == 2
     # batched: negative count
     assert lib.nf4_dequantize_batched(None, -1, 0, None) == 2
+    # fused GEMM: K not a multiple of 64, bad dtypes, misaligned X, both / neither scale modes
+    assert lib.nf4_gemm(fake, 1, 4, fake, fake, None, 128, 100, 64, fake, 1, 0, None, 0, None) == 2
+    assert lib.nf4_gemm(fake, 2, 4, fake, fake, None, 128, 128, 64, fake, 1, 0, None, 0, None) == 4
+    assert lib.nf4_gemm(fake, 1, 4, fake, fake, None, 128, 128, 64, fake, 7, 0, None, 0, None) == 4
+    assert lib.nf4_gemm(P(0x1008), 1, 4, fake, fake, None, 128, 128, 64, fake, 1, 0, None, 0, None) == 5
+    assert lib.nf4_gemm(fake, 1, 4, fake, None, None, 128, 128, 64, fake, 1, 0, None, 0, None) == 6
+    assert lib.nf4_gemm(fake, 1, 4, fake, fake, None, 128, 128, 48, fake, 1, 0, None, 0, None) == 3
+    assert lib.nf4_gemm(fake, 1, 0, fake, fake, None, 128, 128, 64, fake, 1, 0, None, 0, None) == 0   # M == 0
+    # grouped GEMM: count outside [1, 4], NULL table, a member with neither scale mode
+    from paper_2604_02556_b200._lib import GemmWeight
+    ws = (GemmWeight * 5)()
+    for w in ws:
+        w.packed, w.absmax, w.N, w.y = fake, fake, 128, fake
+    assert lib.nf4_gemm_grouped(fake, 1, 4, 128, 64, ws, 0, 1, None, 0, None) == 2
+    assert lib.nf4_gemm_grouped(fake, 1, 4, 128, 64, ws, 5, 1, None, 0, None) == 2
+    assert lib.nf4_gemm_grouped(fake, 1, 4, 128, 64, None, 2, 1, None, 0, None) == 1
+    ws[1].absmax = None
+    assert lib.nf4_gemm_grouped(fake, 1, 4, 128, 64, ws, 2, 1, None, 0, None) == 6   # dq state unset (blocksize2 0)
+    ws[1].dq.blocksize2 = 256
+    assert lib.nf4_gemm_grouped(fake, 1, 4, 128, 64, ws, 2, 1, None, 0, None) == 1   # dq with NULL pointers
+    assert lib.nf4_gemm_grouped_workspace_bytes(4, None, 2, 128) == 0
 
 
 def test_binding_raises_loudly_without_library(tmp_path, monkeypatch):
