@@ -186,7 +186,10 @@ def gemm_reference(x16: np.ndarray, x_dtype: int, packed, N: int, K: int, blocks
     of the NF4 weight [N, K] into x's 16-bit type (bit-exact hot-path values), then
     Y = X . W^T with numpy in fp64 (a library matmul as one step).  Returns
     (Y fp64 [M, N], S fp64 [M, N] = sum_k |x_mk w_nk|) -- S bounds the fp32
-    accumulation error of any summation order: |Y_gpu - Y| <= K * 2^-23 * S."""
+    accumulation error of any summation order: |Y_gpu - Y| <= K * 2^-23 * S.
+    Pinned (tests/test_oracle_pins.py): one-hot / all-ones X against the rounded
+    codebook (closed form), exact linearity for integer X, S >= |Y| and S == Y for
+    non-negative operands."""
     import ml_dtypes
     w16 = dequantize(packed, N * K, blocksize, x_dtype, threads=8, **scale_kw)
     np16 = np.float16 if x_dtype == OUT_F16 else ml_dtypes.bfloat16

@@ -511,3 +511,57 @@ def test_custom_codebook_bruteforce(orc, dtype):
         absmax = syn.hash_absmax(n + 5, 0, -(-n // 128))
         got = orc.dequantize(packed, n, 128, code, absmax=absmax, codebook=cb)
         assert np.array_equal(got, npref.dequant_np(packed, n, 128, dtype, absmax=absmax, codebook=cb))
+
+
+# --------------------------------------------------------------------------
+# F1 reference (oracle.gemm_reference): Y = X . W^T over the oracle's weights
+# --------------------------------------------------------------------------
+def _codebook_rows(N, K):
+    """Row n holds codes (n + k) mod 16 (high nibble first); absmax 1.0 everywhere."""
+    codes = (np.arange(N)[:, None] + np.arange(K)[None, :]) % 16
+    flat = codes.reshape(-1).astype(np.uint8)
+    return (flat[0::2] << 4 | flat[1::2]).astype(np.uint8), codes
+
+
+@pytest.mark.parametrize("x_dtype", ["bf16", "f16"])
+def test_gemm_reference_one_hot_and_ones(orc, x_dtype):
+    """Closed forms independent of the oracle's C: with absmax 1 every weight is
+    RNE16(NF4[code]) (ml_dtypes / numpy rounding of the pinned table), so a one-hot
+    row of X returns one weight and an all-ones row returns the row sum."""
+    N, K = 5, 128
+    packed, codes = _codebook_rows(N, K)
+    absmax = np.ones(N * K // 64, np.float32)
+    np16 = ml_dtypes.bfloat16 if x_dtype == "bf16" else np.float16
+    code = orc.OUT_BF16 if x_dtype == "bf16" else orc.OUT_F16
+    w = orc.codebook().astype(np16).astype(np.float64)[codes]          # [N, K]
+    ks = np.array([0, 7, 64, 127])
+    x = np.zeros((len(ks) + 1, K), np.float32)
+    x[np.arange(len(ks)), ks] = 1.0
+    x[-1, :] = 1.0
+    x16 = x.astype(np16).view(np.uint16)
+    y, s = orc.gemm_reference(x16, code, packed, N, K, 64, absmax=absmax)
+    assert np.array_equal(y[:-1], w[:, ks].T)
+    assert np.array_equal(y[-1], w.sum(axis=1))
+    assert np.array_equal(s[-1], np.abs(w).sum(axis=1))
+
+
+def test_gemm_reference_linearity_and_magnitude(orc):
+    """Integer-valued X keeps every fp64 product and sum exact (|values| < 2^53), so
+    the reference must be exactly linear in X; S = |X|.|W|^T bounds |Y| and equals
+    Y for non-negative X and W."""
+    N, K = 6, 256
+    packed = syn.hash_packed(41, 0, N * K // 2)
+    absmax = np.full(N * K // 64, 2.0, np.float32)
+    rng = np.random.default_rng(5)
+    x1 = rng.integers(-8, 9, (3, K)).astype(np.float32)
+    x2 = rng.integers(-8, 9, (3, K)).astype(np.float32)
+    b = lambda a: a.astype(ml_dtypes.bfloat16).view(np.uint16)       # noqa: E731 (exact for |v| <= 256)
+    y1, s1 = orc.gemm_reference(b(x1), orc.OUT_BF16, packed, N, K, 64, absmax=absmax)
+    y2, _ = orc.gemm_reference(b(x2), orc.OUT_BF16, packed, N, K, 64, absmax=absmax)
+    y12, _ = orc.gemm_reference(b(x1 + x2), orc.OUT_BF16, packed, N, K, 64, absmax=absmax)
+    assert np.array_equal(y12, y1 + y2)
+    assert (np.abs(y1) <= s1).all()
+    # non-negative weights: codes 8..15 only (NF4 >= 0 there), non-negative X -> S == Y
+    pos = (syn.hash_packed(42, 0, N * K // 2) | 0x88).astype(np.uint8)
+    yp, sp = orc.gemm_reference(b(np.abs(x1)), orc.OUT_BF16, pos, N, K, 64, absmax=absmax)
+    assert np.array_equal(yp, sp)
