@@ -770,11 +770,32 @@ __global__ void nf4_gemm_reduce_kernel(const float* __restrict__ partial, int sp
 //   BN 16: 24 KB x 6;  BN 32: 32 KB x 6;  BN 64: 48 KB x 4;  BN 128: 40 KB x 4;
 //   BN 256: 36 KB x 5 (one accumulator: 256 + 3*32 TMEM columns)
 constexpr int kGroups = 3;
-template <int BN> constexpr int sub_for() { return BN <= 64 ? 4 : BN <= 128 ? 2 : 1; }
+// (macros: tuning experiments only, tools/)
 #ifndef NF4_GEMM_CST_SMALL
 #define NF4_GEMM_CST_SMALL 6
 #endif
-template <int BN> constexpr int cst_for() { return BN <= 16 ? NF4_GEMM_CST_SMALL : BN <= 32 ? 6 : BN <= 128 ? 4 : 5; }
+#ifndef NF4_GEMM_SUB64
+#define NF4_GEMM_SUB64 4
+#endif
+#ifndef NF4_GEMM_CST64
+#define NF4_GEMM_CST64 4
+#endif
+#ifndef NF4_GEMM_SUB128
+#define NF4_GEMM_SUB128 2
+#endif
+#ifndef NF4_GEMM_CST128
+#define NF4_GEMM_CST128 4
+#endif
+template <int BN> constexpr int sub_for() {
+  return BN <= 32 ? 4 : BN <= 64 ? NF4_GEMM_SUB64 : BN <= 128 ? NF4_GEMM_SUB128 : 1;
+}
+template <int BN> constexpr int cst_for() {
+  return BN <= 16 ? NF4_GEMM_CST_SMALL : BN <= 32 ? 6 : BN <= 64 ? NF4_GEMM_CST64 : BN <= 128 ? NF4_GEMM_CST128 : 5;
+}
+static int sub_of(int bn) {
+  return bn <= 16 ? sub_for<16>() : bn <= 32 ? sub_for<32>() : bn <= 64 ? sub_for<64>() : bn <= 128 ? sub_for<128>()
+                                                                                            : sub_for<256>();
+}
 template <int BN> constexpr int nacc_for() { return BN <= 128 ? 2 : 1; }
 constexpr int threads_for() { return 32 * (8 * kGroups + 2); }
 
@@ -1082,7 +1103,7 @@ static nf4_status gemm_run(const void* x, nf4_dtype x_dtype, int32_t M, int32_t 
   p.K = K;
   p.Npad = int32_t(npad);
   p.bs_shift = log2i(blocksize);
-  const int sub = bn <= 64 ? 4 : bn <= 128 ? 2 : 1;
+  const int sub = sub_of(bn);
   {
     // whole super-stages per split (SUB chunks share one TMA box); splits = non-empty ranges
     int cps = (nk + splits - 1) / splits;
