@@ -4,35 +4,30 @@
 //
 // The weight never exists in HBM as 16-bit: producer warps read the packed
 // codes (0.5 B/elt) + scales, dequantize them with exactly the hot path's
-// per-element definition (RNE16(fl32(NF4[idx] * a))) straight into
-// shared memory in the UMMA canonical K-major SWIZZLE_128B layout, and one
-// elected thread issues tcgen05.mma (kind::f16, fp32 accumulation in TMEM).
-// The paper motivates exactly this step: dequantization is 72.4% of the
-// quantized matmul and the fused, preprocessing-free direction is the
-// one it leaves open.
+// per-element definition (RNE16(fl32(NF4[idx] * a))) and write the
+// 16-bit weights straight into TMEM, where tcgen05.mma (kind::f16, fp32
+// accumulation in TMEM) reads them as its A operand.  The paper motivates
+// exactly this step: dequantization is 72.4% of the quantized matmul
+// and the fused, preprocessing-free direction is the one it leaves open.
 //
-// Roles (320 threads):
-//   warp 9     TMA issuer (one lane): per super-stage (SUB 64-element chunks)
-//              one 2-D TMA box of packed codes (128 rows x SUB*32 B, swizzled)
-//              and SUB boxes of X (BN rows x 64, SWIZZLE_128B: directly in the
-//              UMMA canonical layout, zero-filled past M).
-//   warps 0-7  producers: thread (w, l) owns weight row 32(w%4)+l (= TMEM lane)
-//              and half w/4 of every chunk; it dequantizes 32 weights and
-//              writes them to TMEM with tcgen05.st -- the A operand of the MMA.
-//              At the end of each segment they are the epilogue (tcgen05.ld).
-//   warp 8     TMEM allocator and MMA issuer: tcgen05.mma.kind::f16 with A in
-//              TMEM and B (X) in shared memory, tcgen05.commit to the barriers.
+// One CTA per SM, 832 threads (see the kernel's comment for details):
+//   warps 0-23  three producer groups of 8 warps; group g dequantizes the
+//               super-stages J = g (mod 3) of the CTA's work into its TMEM A
+//               tiles, and the group that finished a segment runs its epilogue
+//               (tcgen05.ld -> y, or an fp32 partial + per-tile counter).
+//   warp 24     TMEM allocator and MMA issuer (converged warp, elect.sync).
+//   warp 25     TMA issuer: per super-stage (4 chunks of 64 k) one swizzled box
+//               of codes (128 rows x 128 B) and 4 boxes of X (BN x 64, SW128:
+//               the UMMA canonical layout, zero-filled past M).
 // Swap-AB orientation: the MMA's M=128 side is the weight (128 output
 // features), its N side the tokens (BN in {16,...,256}), so decode-size M
 // wastes nothing.
 // Work distribution (stream-K): the (tile, 64-element k-chunk) stream of the
-// whole GEMM is cut into gridDim.x equal contiguous ranges, one per resident
-// CTA (SMs x CTAs/SM), so every SM gets the same work and no second, partial
-// wave exists; a CTA's range covers 1-3 "segments" (a tile's k-sub-range),
-// each accumulated in TMEM and written as an fp32 partial; nf4_gemm_reduce
-// sums a tile's partials in segment order (deterministic for a given GPU).
-// The classic grid (one CTA per tile x split, explicit `splits`) is the same
-// kernel with one segment per CTA.
+// whole GEMM -- or of up to 4 weights sharing X (nf4_gemm_grouped) -- is cut
+// into one equal contiguous range per SM; a tile cut across ranges is summed,
+// in piece order, by the CTA holding its last piece (deterministic for a given
+// GPU).  The classic grid (explicit `splits`, one CTA per tile x split, plus a
+// reduction kernel) is the same kernel with one segment per CTA.
 #include <cuda.h>  // CUtensorMap (the encoder is fetched at run time; no libcuda link)
 #include <cuda_runtime.h>
 #include <stdint.h>
