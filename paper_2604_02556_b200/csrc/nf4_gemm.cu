@@ -334,21 +334,25 @@ struct Scales {
 //                  32(w%4)+l (= TMEM lane) and half (w%8)/4 of each chunk;
 //                  the group that produced a segment's last super-stage then
 //                  runs its epilogue (tcgen05.ld -> y or fp32 partial).
-//   warp 8G        TMEM allocator + MMA issuer (one lane).
+//   warp 8G        TMEM allocator + MMA issuer (the converged warp runs the
+//                  loop; elect.sync picks the issuing lane).
 //   warp 8G+1      TMA issuer (one lane).
 // TMEM: NACC accumulators of max(BN, 32) fp32 columns, then G*SUB A tiles of
 // 32 columns (128 lanes x 64 16-bit weights), one per (group, chunk-in-stage).
-// Barriers (one arrive/commit per super-stage each, so the single MMA thread
-// spends its time issuing MMAs, not waiting on barriers): c_full (TMA bytes) /
+// Barriers (one arrive/commit per super-stage each, so the MMA issuer spends
+// its time issuing MMAs, not waiting on barriers): c_full (TMA bytes) /
 // c_free (MMA commit: the MMA waited for w_full, so the codes were read too)
 // per shared-memory super-stage (CST >= G keeps every parity wait within one
 // phase); w_full (8 warps) / a_free (MMA commit) per group's 4 A tiles;
 // acc_full / acc_empty per accumulator.
 // Stream-K fix-up (no second kernel): every tile piece that is not the tile's
 // last is published as an fp32 partial + a per-tile counter increment; the CTA
-// holding the tile's last piece (its range's first segment) sums the partials
-// in piece order at the end of its range and writes y.  It waits only for
-// lower-numbered CTAs, dispatched before it.
+// holding the tile's last piece (its range's first chunk) sums the partials in
+// piece order at the end of its range and writes y.  It waits only for
+// lower-numbered CTAs, dispatched before it, which compute the head piece of
+// their last tile first (seg_begin), so the wait is normally already over.
+// Grouped GEMMs (MULTI): the segment's member selects the TMA descriptor,
+// scale pointers, code2 table and output.
 template <int BN, int G, int SUB, int CST, int NACC, bool BF16, bool MULTI>
 __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
     nf4_gemm_kernel(const __grid_constant__ GemmParams p, const __grid_constant__ CodeMapsT<MULTI ? kMaxMembers : 1> maps,
