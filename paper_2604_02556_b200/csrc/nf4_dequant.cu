@@ -272,6 +272,11 @@ __global__ void __launch_bounds__(kThreads) dequant_kernel(const __grid_constant
           static_cast<uint32_t>(__cvta_generic_to_shared(&clc_bar[i]))) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // Programmatic dependent launch: the prologue above touches only parameters and
+  // shared memory, so it may overlap the previous kernel's tail; inputs and the
+  // output buffer are touched only after the previous grid has completed.
+  if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
 
   int cur = 0;
@@ -400,6 +405,23 @@ static int current_variant() {
 
 static int64_t tile_elems(int v) { return int64_t(kThreads) * 2 * kVariants[v].vec * kVariants[v].unroll; }
 
+// Launch with programmatic stream serialization (PDL): the kernel executes
+// griddepcontrol.wait before its first global access.
+template <typename Kernel, typename Params>
+static void launch_pdl(Kernel k, int grid, cudaStream_t stream, const Params& P) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, P);   // errors surface through cudaPeekAtLastError at the call site
+}
+
 template <int MAXB>
 static void launch_small(const BatchParams& P, int out, int grid, cudaStream_t stream) {
   BatchParamsT<MAXB> Q;
@@ -409,11 +431,11 @@ static void launch_small(const BatchParams& P, int out, int grid, cudaStream_t s
   for (int i = 0; i < 16; ++i) Q.lut[i] = P.lut[i];
   for (int i = 0; i < P.count; ++i) Q.t[i] = P.t[i];
   if (out == 0)
-    dequant_kernel<0, 8, 4, false, true, true, true, false, MAXB><<<grid, kThreads, 0, stream>>>(Q);
+    launch_pdl(dequant_kernel<0, 8, 4, false, true, true, true, false, MAXB>, grid, stream, Q);
   else if (out == 1)
-    dequant_kernel<1, 8, 4, false, true, true, true, false, MAXB><<<grid, kThreads, 0, stream>>>(Q);
+    launch_pdl(dequant_kernel<1, 8, 4, false, true, true, true, false, MAXB>, grid, stream, Q);
   else
-    dequant_kernel<2, 8, 4, false, true, true, true, false, MAXB><<<grid, kThreads, 0, stream>>>(Q);
+    launch_pdl(dequant_kernel<2, 8, 4, false, true, true, true, false, MAXB>, grid, stream, Q);
 }
 
 static KernelFn kernel_of(int out, int v) {
@@ -499,7 +521,7 @@ static nf4_status launch_batch(const nf4_tensor* ts, int count, int out, const f
     else launch_small<16>(P, out, grid, stream);
   } else {
     KernelFn fn = kernel_of(out, v);
-    fn<<<grid, kThreads, 0, stream>>>(P);
+    launch_pdl(fn, grid, stream, P);
   }
   const cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) {
