@@ -130,6 +130,10 @@ def main():
            "fused_ms": round(fused_ms, 4),
            "fused_hbm_gbs": round((bytes_w + bytes_xy) / (fused_ms * 1e-3) / 1e9, 1),
            "fused_tflops": round(flops / (fused_ms * 1e-3) / 1e12, 2),
+           # roofline of the fused kernel: one shared-memory LUT lookup per weight,
+           # 6.48 T lookups/s measured on this GPU (profiles/r01_lutbench.txt)
+           "fused_tweights_per_s": round(n_total / (fused_ms * 1e-3) / 1e12, 3),
+           "frac_of_lut_bound": round(n_total / (fused_ms * 1e-3) / 6.48e12, 3),
            "splits": sorted(set(splits.values())), "grouped": bool(args.grouped),
            "launches_per_step": len(groups) if args.grouped else len(tensors)}
     if not args.no_unfused:
