@@ -34,6 +34,13 @@
  *            concurrent calls).  Results are deterministic for a given
  *            (splits, GPU).
  * Stream-ordered, asynchronous; status codes as nf4.h.
+ * Programmatic dependent launch: the kernel may start while the previous
+ * kernel on the stream drains, and it reads the WEIGHT (packed, absmax / dq
+ * and its tables) before waiting for that kernel -- only x, y and the
+ * workspace are ordered after it.  So the weight must not be written by the
+ * immediately preceding kernel when that kernel triggers its dependents early
+ * (none of this library's weight writers -- nf4_quantize,
+ * nf4_double_quantize -- do; any other kernel triggers only at its exit).
  */
 #ifndef NF4_GEMM_H_
 #define NF4_GEMM_H_

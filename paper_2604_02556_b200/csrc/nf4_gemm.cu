@@ -340,8 +340,9 @@ struct Scales {
 // TMEM: NACC accumulators of max(BN, 32) fp32 columns, then G*SUB A tiles of
 // 32 columns (128 lanes x 64 16-bit weights), one per (group, chunk-in-stage).
 // Barriers (one arrive/commit per super-stage each, so the MMA issuer spends
-// its time issuing MMAs, not waiting on barriers): c_full (TMA bytes) /
-// c_free (MMA commit: the MMA waited for w_full, so the codes were read too)
+// its time issuing MMAs, not waiting on barriers): c_full (code bytes), x_full
+// (X bytes) / c_free (MMA commit: the MMA waited for w_full, so the codes were
+// read too)
 // per shared-memory super-stage (CST >= G keeps every parity wait within one
 // phase); w_full (8 warps) / a_free (MMA commit) per group's 4 A tiles;
 // acc_full / acc_empty per accumulator.
@@ -368,7 +369,8 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ __align__(256) float lut[16];                    // 256-B aligned: address = PRMT(offsets, base)
   __shared__ float code2s[kMem][256];                         // DQ second-level tables
-  __shared__ __align__(8) uint64_t c_full[CST], c_free[CST], w_full[G], a_free[G], acc_full[NACC], acc_empty[NACC];
+  __shared__ __align__(8) uint64_t c_full[CST], x_full[CST], c_free[CST], w_full[G], a_free[G], acc_full[NACC],
+      acc_empty[NACC];
   __shared__ uint32_t tmem_holder;
   __shared__ int sk_range[3];                                 // stream-K: range start, end, first slot
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -387,6 +389,7 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < CST; ++s) {
       mbar_init(&c_full[s], 1);
+      mbar_init(&x_full[s], 1);
       mbar_init(&c_free[s], 1);
     }
     for (int s = 0; s < G; ++s) {
@@ -419,10 +422,14 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_x)) : "memory");
   }
   // Programmatic dependent launch: the next kernel in the stream may start its own
-  // prologue as soon as our CTAs leave their SMs; everything above touches only
-  // parameters and on-chip state, so it overlaps the previous kernel's tail.
+  // prologue as soon as our CTAs leave their SMs.  Only X, y and the workspace
+  // can depend on the previous kernel: the weight (codes, scales, code2) is
+  // read BEFORE griddepcontrol.wait (nf4_gemm.h states the contract), so the
+  // TMA warp fetches the first super-stages of codes and the producers
+  // dequantize them into TMEM while the previous kernel drains; the TMA warp
+  // waits before loading X, the producers before their first store to y or
+  // the workspace, everybody before the stream-K fix-up.
   if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");   // inputs (and the workspace) are now ready
   for (int i = 0; i < kMem && i < p.nmem; ++i) {
     if (p.mem[i].absmax == nullptr)
       for (int t = threadIdx.x; t < 256; t += blockDim.x) code2s[i][t] = p.mem[i].code2[t];
@@ -501,7 +508,7 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
         const int Jg = J + j;
         const int cs = Jg % CST;
         const uint32_t aph = uint32_t(Jg / G) & 1u;
-        mbar_wait_parity(&c_full[cs], uint32_t(Jg / CST) & 1u);   // codes + X of this super-stage landed
+        mbar_wait_parity(&c_full[cs], uint32_t(Jg / CST) & 1u);   // codes of this super-stage landed
         if (wl == 0 && lane == 0) NF4_TRACE_J(100, Jg);
         mbar_wait_parity(&a_free[g], aph ^ 1u);                    // the MMA is done with our previous A tiles
         if (wl == 0 && lane == 0) NF4_TRACE_J(200, Jg);
@@ -585,6 +592,7 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
       if (jlast % G == g) {
         const int ab = sidx % NACC;
         mbar_wait_parity(&acc_full[ab], uint32_t(sidx / NACC) & 1u);
+        asm volatile("griddepcontrol.wait;" ::: "memory");   // y / partials / counters: the previous kernel is done
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const int qd = wl & 3;                           // TMEM lane quarter this warp may access
         constexpr int HB = BN / 2 < 16 ? 16 : BN / 2;    // columns per warp (BN = 16: warps 4-7 idle)
@@ -639,26 +647,45 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
 #undef absmax2
   } else if (warp == kTmaWarp) {
     // ======================= TMA issuer (one thread) =======================
+    // Codes of super-stage Jg -> c_full[Jg % CST], X -> x_full[Jg % CST].  The
+    // codes of the first CST super-stages (slots initially free) are issued
+    // before griddepcontrol.wait; X only after it.
     if (lane == 0) {
+      const bool ld_c = !(NF4_EXP(16)), ld_x = !(NF4_EXP(8));
+      auto issue_codes = [&](const Segment& sg, int j, int cs) {
+        asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&c_full[cs])),
+                     "r"(uint32_t(ld_c ? kSuperCodeBytes : 0)) : "memory");
+        if (ld_c) tma_load_2d(smem_c + cs * kSuperCodeBytes, &maps.m[sg.g], (sg.kc0 + j * SUB) * kChunk / 2, sg.n0,
+                              &c_full[cs]);
+      };
       int J = 0;
       SegIter it = seg_begin(p, sk_range);
       Segment sg;
+      while (J < CST && next_segment<BN, MULTI>(p, it, sg)) {
+        const int nsuper = (sg.nk + SUB - 1) / SUB;
+        for (int j = 0; j < nsuper && J + j < CST; ++j) issue_codes(sg, j, J + j);
+        J += nsuper;
+      }
+      asm volatile("griddepcontrol.wait;" ::: "memory");   // X is the previous kernel's output
+      J = 0;
+      it = seg_begin(p, sk_range);
       while (next_segment<BN, MULTI>(p, it, sg)) {
         const int nsuper = (sg.nk + SUB - 1) / SUB;
         for (int j = 0; j < nsuper; ++j) {
           const int Jg = J + j, cs = Jg % CST;
-          mbar_wait_parity(&c_free[cs], (uint32_t(Jg / CST) & 1u) ^ 1u);   // super-stage Jg-CST consumed
+          if (Jg >= CST) {
+            mbar_wait_parity(&c_free[cs], (uint32_t(Jg / CST) & 1u) ^ 1u);   // super-stage Jg-CST consumed
+            issue_codes(sg, j, cs);
+          }
           NF4_TRACE_J(400, Jg);
           const int k0 = (sg.kc0 + j * SUB) * kChunk;
-          const bool ld_c = !(NF4_EXP(16)), ld_x = !(NF4_EXP(8));
           asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
-              smem_u32(&c_full[cs])), "r"(uint32_t((ld_c ? kSuperCodeBytes : 0) + (ld_x ? kSuperXBytes : 0))) : "memory");
-          if (ld_c) tma_load_2d(smem_c + cs * kSuperCodeBytes, &maps.m[sg.g], k0 / 2, sg.n0, &c_full[cs]);
+              smem_u32(&x_full[cs])), "r"(uint32_t(ld_x ? kSuperXBytes : 0)) : "memory");
           if (ld_x) {
 #pragma unroll
             for (int q = 0; q < SUB; ++q)
               tma_load_2d(smem_x + cs * kSuperXBytes + q * BN * kRowBytes, &map_x, k0 + q * kChunk, sg.m0,
-                          &c_full[cs]);
+                          &x_full[cs]);
           }
         }
         J += nsuper;
@@ -678,7 +705,8 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
       const uint32_t d_tmem = tmem + uint32_t(ab * ACC);
       for (int j = 0; j < nsuper; ++j) {
         const int Jg = J + j, g = Jg % G, cs = Jg % CST;
-        mbar_wait_parity(&w_full[g], uint32_t(Jg / G) & 1u);               // A tiles in TMEM (X landed before)
+        mbar_wait_parity(&w_full[g], uint32_t(Jg / G) & 1u);               // A tiles in TMEM
+        mbar_wait_parity(&x_full[cs], uint32_t(Jg / CST) & 1u);            // X of this super-stage landed
         if (lane == 0) NF4_TRACE_J(500, Jg);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if (!(NF4_EXP(1))) {
@@ -703,6 +731,7 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
     }
     __syncwarp();
   }
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // (a no-op for threads that already waited)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (p.streamk) {
