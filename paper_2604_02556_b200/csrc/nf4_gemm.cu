@@ -510,9 +510,6 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
         const uint32_t aph = uint32_t(Jg / G) & 1u;
         mbar_wait_parity(&c_full[cs], uint32_t(Jg / CST) & 1u);   // codes of this super-stage landed
         if (wl == 0 && lane == 0) NF4_TRACE_J(100, Jg);
-        mbar_wait_parity(&a_free[g], aph ^ 1u);                    // the MMA is done with our previous A tiles
-        if (wl == 0 && lane == 0) NF4_TRACE_J(200, Jg);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const int64_t b0 = blk_base + kc0 + 4 * j;
         // the stage body, specialised on "all SUB chunks present" and the scale format
         // (uniform branches hoisted out of the per-chunk code)
@@ -558,6 +555,14 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
                   w[4 * cc + jj] = pack2_rn<BF16>(ch, cl);
                 }
               }
+            }
+            if (q == 0) {
+              // The first chunk is dequantized into registers before this wait, so a
+              // warp that finished its previous super-stage ahead of the rest of its
+              // group (and of the MMA that must release the A tiles) keeps working.
+              mbar_wait_parity(&a_free[g], aph ^ 1u);                // the MMA is done with our previous A tiles
+              if (wl == 0 && lane == 0) NF4_TRACE_J(200, Jg);
+              asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             }
             if (!NF4_EXP(4)) {
               // 16 columns (32 weights) of this row's A tile (group g, chunk q) in TMEM
@@ -637,7 +642,7 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
           __syncwarp();
           if (lane == 0) atomicAdd(p.flags + (sg.m0 / BN) * p.tiles_n + sg.tn, 1u);
         }
-        if (NF4_TRACING && threadIdx.x == 32 * 8 * g) p.trace[1024 + 4 * cta_lin + 3] = gtimer();
+        if (NF4_TRACING && wl == 0 && lane == 0) p.trace[1024 + 4 * cta_lin + 3] = gtimer();
       }
       J += nsuper;
       ++sidx;
