@@ -238,6 +238,22 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* m
       : "memory");
 }
 
+// Byte-pair lookup table (NF4_GEMM_PAIR): entry b = (NF4[b >> 4], NF4[b & 15]),
+// the two fp32 levels of one code byte (element 2j, element 2j+1), replicated
+// once per lane: row b (256 B) holds 32 copies, lane l reads its copy at l*8, so
+// the 16 lanes of each LDS.64 phase hit 16 distinct bank pairs for any codes
+// (conflict-free), and the address of byte j of a code word is ONE PRMT
+// (byte j -> bits 8-15, lane*8 -> bits 0-7) plus the table base folded into the
+// LDS.  Per two weights: PRMT + LDS.64 + FMUL2 + F2FP.
+#ifndef NF4_GEMM_PAIR
+#define NF4_GEMM_PAIR 1
+#endif
+#ifndef NF4_GEMM_PAIR_MAXBN
+#define NF4_GEMM_PAIR_MAXBN 64   // wider token tiles need the shared memory for X stages
+#endif
+template <int BN> __host__ __device__ constexpr bool pair_for() { return NF4_GEMM_PAIR && BN <= NF4_GEMM_PAIR_MAXBN; }
+template <int BN> __host__ __device__ constexpr int pair_table_bytes() { return pair_for<BN>() ? 256 * 256 : 0; }
+
 // Code-box swizzle: the TMA writes the 128 rows x (SUB*32) B box with the
 // hardware swizzle matching its width, so the 8 lanes of an LDS.128 phase
 // (consecutive rows, same 16-B column) hit 8 different bank groups.
@@ -374,7 +390,8 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
   __shared__ uint32_t tmem_holder;
   __shared__ int sk_range[3];                                 // stream-K: range start, end, first slot
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* smem_c = smem;                                     // CST x 128 rows x SUB*32 B (codes)
+  uint8_t* ptab = smem;                                       // NF4_GEMM_PAIR: 256 rows x 32 lanes x 8 B
+  uint8_t* smem_c = smem + pair_table_bytes<BN>();            // CST x 128 rows x SUB*32 B (codes)
   uint8_t* smem_x = smem_c + CST * kSuperCodeBytes;           // CST x SUB x BN x 128 B (X)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -386,6 +403,14 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
     p.trace[1024 + 4 * cta_lin + 2] = smid;
   }
   if (threadIdx.x < 16) lut[threadIdx.x] = p.lut[threadIdx.x];
+  if constexpr (pair_for<BN>()) {
+    // row b: 32 copies of (NF4[b >> 4], NF4[b & 15]); 16-B stores of two copies
+    for (int i = threadIdx.x; i < 256 * 16; i += blockDim.x) {
+      const int b = i >> 4;
+      const float h = p.lut[b >> 4], l = p.lut[b & 15];
+      *reinterpret_cast<float4*>(ptab + 16 * i) = make_float4(h, l, h, l);
+    }
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < CST; ++s) {
       mbar_init(&c_full[s], 1);
@@ -448,6 +473,8 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
     const int chunk_shift = p.bs_shift - 6;    // 64-element chunks per quantization block = 2^chunk_shift
     const uint32_t tlane = uint32_t(32 * (wl & 3)) << 16;
     const uint32_t lut_base = smem_u32(lut);   // low byte 0: PRMT splices a byte offset into it
+    const uint32_t ptab_base = smem_u32(ptab);
+    const uint32_t lane8 = uint32_t(lane) * 8u;
     int J = 0, sidx = 0;                       // super-stages / segments before this segment
     SegIter it = seg_begin(p, sk_range);
     Segment sg;
@@ -538,6 +565,22 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
               // dequantize 32 weights: word jj = (element 2jj) | (element 2jj+1) << 16
               const uint32_t cw[4] = {c0.x, c0.y, c0.z, c0.w};
               const uint64_t aa = f32x2_splat(a);
+              if constexpr (pair_for<BN>()) {
+#pragma unroll
+                for (int cc = 0; cc < 4; ++cc) {
+#pragma unroll
+                  for (int jj = 0; jj < 4; ++jj) {
+                    // (byte jj of the word) * 256 + lane * 8: one PRMT
+                    const uint32_t off = __byte_perm(cw[cc], lane8, 0x7604u + 16u * jj);
+                    uint64_t v, r;
+                    asm("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(ptab_base + off));
+                    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(v), "l"(aa));   // fl32(NF4[idx] * a), both
+                    float ch, cl;
+                    asm("mov.b64 {%0, %1}, %2;" : "=f"(ch), "=f"(cl) : "l"(r));
+                    w[4 * cc + jj] = pack2_rn<BF16>(ch, cl);
+                  }
+                }
+              } else {
 #pragma unroll
               for (int cc = 0; cc < 4; ++cc) {
                 const uint32_t x = cw[cc];
@@ -554,6 +597,7 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
                   mul2_rn(ch, cl, aa);                      // fl32(NF4[idx] * a) for both, one FMUL2
                   w[4 * cc + jj] = pack2_rn<BF16>(ch, cl);
                 }
+              }
               }
             }
             if (q == 0) {
@@ -823,7 +867,10 @@ template <int BN> constexpr int sub_for() {
   return BN <= 32 ? 4 : BN <= 64 ? NF4_GEMM_SUB64 : BN <= 128 ? NF4_GEMM_SUB128 : 1;
 }
 template <int BN> constexpr int cst_for() {
-  return BN <= 16 ? NF4_GEMM_CST_SMALL : BN <= 32 ? 6 : BN <= 64 ? NF4_GEMM_CST64 : BN <= 128 ? NF4_GEMM_CST128 : 5;
+  // with the 64 KB pair table: 6 / 4 / 3 / 3 / 4 stages fit in 227 KB
+  return pair_for<BN>() ? (BN <= 16 ? NF4_GEMM_CST_SMALL : BN <= 32 ? 4 : BN <= 64 ? 3 : BN <= 128 ? 3 : 4)
+                        : (BN <= 16 ? NF4_GEMM_CST_SMALL : BN <= 32 ? 6 : BN <= 64 ? NF4_GEMM_CST64
+                                                                       : BN <= 128 ? NF4_GEMM_CST128 : 5);
 }
 static int sub_of(int bn) {
   return bn <= 16 ? sub_for<16>() : bn <= 32 ? sub_for<32>() : bn <= 64 ? sub_for<64>() : bn <= 128 ? sub_for<128>()
@@ -834,7 +881,7 @@ constexpr int threads_for() { return 32 * (8 * kGroups + 2); }
 
 template <int BN>
 constexpr size_t smem_bytes() {
-  return 1024 /*align slack*/ + size_t(cst_for<BN>()) * sub_for<BN>() * (128 * kCodeBytes + BN * kRowBytes);
+  return 1024 /*align slack*/ + pair_table_bytes<BN>() + size_t(cst_for<BN>()) * sub_for<BN>() * (128 * kCodeBytes + BN * kRowBytes);
 }
 
 template <int BN, bool BF16, bool MULTI>
