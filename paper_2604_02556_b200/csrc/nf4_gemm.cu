@@ -240,19 +240,23 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* m
 
 // Byte-pair lookup table (NF4_GEMM_PAIR): entry b = (NF4[b >> 4], NF4[b & 15]),
 // the two fp32 levels of one code byte (element 2j, element 2j+1), replicated
-// once per lane: row b (256 B) holds 32 copies, lane l reads its copy at l*8, so
-// the 16 lanes of each LDS.64 phase hit 16 distinct bank pairs for any codes
-// (conflict-free), and the address of byte j of a code word is ONE PRMT
-// (byte j -> bits 8-15, lane*8 -> bits 0-7) plus the table base folded into the
-// LDS.  Per two weights: PRMT + LDS.64 + FMUL2 + F2FP.
+// once per lane of a half-warp: row b (NF4_GEMM_PAIR_ROW = 128 B) holds 16
+// copies, lane l reads copy l % 16, so the 16 lanes of each LDS.64 phase (a
+// 64-bit load is served per half-warp) hit 16 distinct bank pairs for any
+// codes: conflict-free.  (ROW 256: 32 copies, lane l reads copy l.)  The
+// address of byte j of a code word is one PRMT (ALU) + one IMAD (FMA pipe).
+// Per two weights: PRMT + IMAD + LDS.64 + FMUL2 + F2FP.
 #ifndef NF4_GEMM_PAIR
 #define NF4_GEMM_PAIR 1
 #endif
 #ifndef NF4_GEMM_PAIR_MAXBN
-#define NF4_GEMM_PAIR_MAXBN 64   // wider token tiles need the shared memory for X stages
+#define NF4_GEMM_PAIR_MAXBN 256
+#endif
+#ifndef NF4_GEMM_PAIR_ROW
+#define NF4_GEMM_PAIR_ROW 128
 #endif
 template <int BN> __host__ __device__ constexpr bool pair_for() { return NF4_GEMM_PAIR && BN <= NF4_GEMM_PAIR_MAXBN; }
-template <int BN> __host__ __device__ constexpr int pair_table_bytes() { return pair_for<BN>() ? 256 * 256 : 0; }
+template <int BN> __host__ __device__ constexpr int pair_table_bytes() { return pair_for<BN>() ? 256 * NF4_GEMM_PAIR_ROW : 0; }
 
 // Code-box swizzle: the TMA writes the 128 rows x (SUB*32) B box with the
 // hardware swizzle matching its width, so the 8 lanes of an LDS.128 phase
@@ -404,9 +408,10 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
   }
   if (threadIdx.x < 16) lut[threadIdx.x] = p.lut[threadIdx.x];
   if constexpr (pair_for<BN>()) {
-    // row b: 32 copies of (NF4[b >> 4], NF4[b & 15]); 16-B stores of two copies
-    for (int i = threadIdx.x; i < 256 * 16; i += blockDim.x) {
-      const int b = i >> 4;
+    // row b: ROW/8 copies of (NF4[b >> 4], NF4[b & 15]); 16-B stores of two copies
+    constexpr int kStoresPerRow = NF4_GEMM_PAIR_ROW / 16;
+    for (int i = threadIdx.x; i < 256 * kStoresPerRow; i += blockDim.x) {
+      const int b = i / kStoresPerRow;
       const float h = p.lut[b >> 4], l = p.lut[b & 15];
       *reinterpret_cast<float4*>(ptab + 16 * i) = make_float4(h, l, h, l);
     }
@@ -474,7 +479,7 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
     const uint32_t tlane = uint32_t(32 * (wl & 3)) << 16;
     const uint32_t lut_base = smem_u32(lut);   // low byte 0: PRMT splices a byte offset into it
     const uint32_t ptab_base = smem_u32(ptab);
-    const uint32_t lane8 = uint32_t(lane) * 8u;
+    const uint32_t ptab_lane = ptab_base + uint32_t(lane % (NF4_GEMM_PAIR_ROW / 8)) * 8u;
     int J = 0, sidx = 0;                       // super-stages / segments before this segment
     SegIter it = seg_begin(p, sk_range);
     Segment sg;
@@ -570,10 +575,10 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
                 for (int cc = 0; cc < 4; ++cc) {
 #pragma unroll
                   for (int jj = 0; jj < 4; ++jj) {
-                    // (byte jj of the word) * 256 + lane * 8: one PRMT
-                    const uint32_t off = __byte_perm(cw[cc], lane8, 0x7604u + 16u * jj);
+                    // row of byte jj of the word, this lane's copy
+                    const uint32_t byte = __byte_perm(cw[cc], 0u, 0x4440u + jj);
                     uint64_t v, r;
-                    asm("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(ptab_base + off));
+                    asm("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(ptab_lane + byte * NF4_GEMM_PAIR_ROW));
                     asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(v), "l"(aa));   // fl32(NF4[idx] * a), both
                     float ch, cl;
                     asm("mov.b64 {%0, %1}, %2;" : "=f"(ch), "=f"(cl) : "l"(r));
@@ -867,8 +872,10 @@ template <int BN> constexpr int sub_for() {
   return BN <= 32 ? 4 : BN <= 64 ? NF4_GEMM_SUB64 : BN <= 128 ? NF4_GEMM_SUB128 : 1;
 }
 template <int BN> constexpr int cst_for() {
-  // with the 64 KB pair table: 6 / 4 / 3 / 3 / 4 stages fit in 227 KB
-  return pair_for<BN>() ? (BN <= 16 ? NF4_GEMM_CST_SMALL : BN <= 32 ? 4 : BN <= 64 ? 3 : BN <= 128 ? 3 : 4)
+  // with the 32 KB pair table: 6 / 5 / 3 / 4 / 5 stages fit in 227 KB (64 KB table: 6 / 4 / 3 / 3 / 4)
+  return pair_for<BN>() ? (NF4_GEMM_PAIR_ROW == 128
+                               ? (BN <= 16 ? NF4_GEMM_CST_SMALL : BN <= 32 ? 5 : BN <= 64 ? 3 : BN <= 128 ? 4 : 5)
+                               : (BN <= 16 ? NF4_GEMM_CST_SMALL : BN <= 32 ? 4 : BN <= 64 ? 3 : BN <= 128 ? 3 : 4))
                         : (BN <= 16 ? NF4_GEMM_CST_SMALL : BN <= 32 ? 6 : BN <= 64 ? NF4_GEMM_CST64
                                                                        : BN <= 128 ? NF4_GEMM_CST128 : 5);
 }
