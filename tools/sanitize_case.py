@@ -79,6 +79,19 @@ def main():
     torch.cuda.synchronize()
     ref2, mag2 = oracle.gemm_reference(x2_16, oracle.OUT_BF16, wp2, N2, K2, 64, **kw2)
     bad += int(not (np.abs(y2.cpu().numpy().astype(np.float64) - ref2) <= K2 * 2.0 ** -23 * mag2 + 1e-30).all())
+    # grouped GEMM (2 members) at three token-tile widths, launched back to back (programmatic
+    # dependent launch: the weights are read before griddepcontrol.wait); bit-identical to
+    # the single-weight launches
+    wp3 = d(syn.hash_packed(11, 0, 256 * 256 // 2))
+    wa3 = d(syn.hash_absmax(11, 0, 256 * 256 // 64))
+    for Mg in (5, 100, 200):
+        xg = torch.randn(Mg, 256, device="cuda").to(torch.bfloat16)
+        for _ in range(2):
+            yg = nf4.nf4_gemm_grouped(xg, [(wp, wa, None, 128), (wp3, wa3, None, 256)], K=256, y_dtype="f32")
+        y0 = nf4.nf4_gemm(xg, wp, wa, None, N=128, K=256, y_dtype="f32")
+        y1 = nf4.nf4_gemm(xg, wp3, wa3, None, N=256, K=256, y_dtype="f32")
+        torch.cuda.synchronize()
+        bad += int(not (torch.equal(yg[0], y0) and torch.equal(yg[1], y1)))
     # synth + sol
     buf8 = torch.empty(8192 * 4, dtype=torch.uint8, device="cuda")
     nf4.nf4_synth_fill(_lib.NF4_SYNTH_CODES, 1, 3, 1000, buf8)
