@@ -849,15 +849,16 @@ __global__ void nf4_gemm_reduce_kernel(const float* __restrict__ partial, int sp
 }
 // Per token-tile width: G producer groups, SUB chunks per super-stage (code box
 // width SUB*32 B), CST super-stages in shared memory, NACC accumulators in TMEM.
-//   BN 16: 24 KB x 6;  BN 32: 32 KB x 6;  BN 64: 48 KB x 4;  BN 128: 40 KB x 4;
-//   BN 256: 36 KB x 5 (one accumulator: 256 + 3*32 TMEM columns)
+// With the 32 KB byte-pair table: BN 16: 24 KB x 6;  BN 32: 32 KB x 5;
+//   BN 64: 24 KB (2 chunks) x 6;  BN 128: 40 KB (2 chunks) x 4;  BN 256: 36 KB
+//   (1 chunk) x 5 (one accumulator: 256 + 3*32 TMEM columns).
 constexpr int kGroups = 3;
 // (macros: tuning experiments only, tools/)
 #ifndef NF4_GEMM_CST_SMALL
 #define NF4_GEMM_CST_SMALL 6
 #endif
 #ifndef NF4_GEMM_SUB64
-#define NF4_GEMM_SUB64 4
+#define NF4_GEMM_SUB64 2
 #endif
 #ifndef NF4_GEMM_CST64
 #define NF4_GEMM_CST64 4
@@ -868,13 +869,26 @@ constexpr int kGroups = 3;
 #ifndef NF4_GEMM_CST128
 #define NF4_GEMM_CST128 4
 #endif
+#ifndef NF4_GEMM_SUB32
+#define NF4_GEMM_SUB32 4
+#endif
+#ifndef NF4_GEMM_PCST32
+#define NF4_GEMM_PCST32 5
+#endif
+#ifndef NF4_GEMM_PCST64
+#define NF4_GEMM_PCST64 6
+#endif
+#ifndef NF4_GEMM_PCST128
+#define NF4_GEMM_PCST128 4
+#endif
 template <int BN> constexpr int sub_for() {
-  return BN <= 32 ? 4 : BN <= 64 ? NF4_GEMM_SUB64 : BN <= 128 ? NF4_GEMM_SUB128 : 1;
+  return BN <= 16 ? 4 : BN <= 32 ? NF4_GEMM_SUB32 : BN <= 64 ? NF4_GEMM_SUB64 : BN <= 128 ? NF4_GEMM_SUB128 : 1;
 }
 template <int BN> constexpr int cst_for() {
-  // with the 32 KB pair table: 6 / 5 / 3 / 4 / 5 stages fit in 227 KB (64 KB table: 6 / 4 / 3 / 3 / 4)
+  // with the 32 KB pair table: 6 / 5 / 6 (2-chunk) / 4 / 5 stages fit in 227 KB (64 KB table: 6 / 4 / 3 / 3 / 4)
   return pair_for<BN>() ? (NF4_GEMM_PAIR_ROW == 128
-                               ? (BN <= 16 ? NF4_GEMM_CST_SMALL : BN <= 32 ? 5 : BN <= 64 ? 3 : BN <= 128 ? 4 : 5)
+                               ? (BN <= 16 ? NF4_GEMM_CST_SMALL : BN <= 32 ? NF4_GEMM_PCST32 : BN <= 64 ? NF4_GEMM_PCST64
+                                                                : BN <= 128 ? NF4_GEMM_PCST128 : 5)
                                : (BN <= 16 ? NF4_GEMM_CST_SMALL : BN <= 32 ? 4 : BN <= 64 ? 3 : BN <= 128 ? 3 : 4))
                         : (BN <= 16 ? NF4_GEMM_CST_SMALL : BN <= 32 ? 6 : BN <= 64 ? NF4_GEMM_CST64
                                                                        : BN <= 128 ? NF4_GEMM_CST128 : 5);
