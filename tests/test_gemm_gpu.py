@@ -64,7 +64,10 @@ def test_gemm_weights_bit_exact_via_one_hot(nf4, orc, xdt, dq):
     # splits 0 = stream-K: (16, 5120, 448) has 7 chunks per tile (ranges not 4-aligned,
     # tiles cut into up to 7 segments); (300, 256, 1280) two token tiles, 5 segments each
     cases = ((16, 256, 512, 64, 1), (5, 384, 1024, 128, 3), (40, 200, 640, 64, 2),
-             (16, 256, 512, 64, 0), (40, 200, 640, 64, 0), (16, 5120, 448, 64, 0), (300, 256, 1280, 64, 0))
+             (16, 256, 512, 64, 0), (40, 200, 640, 64, 0), (16, 5120, 448, 64, 0), (300, 256, 1280, 64, 0),
+             # every token-tile width (BN 32 / 64 with 2-chunk stages / 128) through the byte-pair
+             # table, stream-K, incl. the general (per-chunk) scale path at blocksize 128
+             (24, 384, 768, 64, 0), (50, 256, 1024, 128, 0), (100, 256, 1024, 64, 0))
     for (M, N, K, bs, splits) in cases:
         packed, kw = _weights(N, K, bs, dq, seed=M + N + K)
         ks = (np.arange(M) * 37 + 11) % K
@@ -200,7 +203,7 @@ def test_gemm_stream_k_workspace_reuse(nf4, orc):
         assert int(ws[:4 * tiles].view(torch.int32).abs().sum()) == 0, "stream-K counters not reset"
 
 
-@pytest.mark.parametrize("M", [5, 16, 40])
+@pytest.mark.parametrize("M", [5, 16, 40, 100])
 def test_gemm_grouped_bit_exact_weights_and_bound(nf4, orc, M):
     """nf4_gemm_grouped: q/k/v-like members (different N, one not a multiple of 128,
     fp32 and double-quant absmax) in one launch; one-hot X checks every member's
