@@ -510,7 +510,16 @@ def run_ours(args, rank, world, local_rank):
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": UNIT,
                          "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
                          "kernel": "nf4::dequant_kernel", "kernel_ms_per_step": round(kernel_ms, 4),
-                         "bytes_per_step": alg_per_step},
+                         "bytes_per_step": alg_per_step,
+                         # SURVEY 8(d) timing protocol over the per-step kernel times of this pass:
+                         # median (the headline `achieved`), min / max, and the paper's
+                         # "mean of 3 measured passes after 1 warm-up"
+                         "per_step_gbs": {"median": round(achieved, 1),
+                                          "best": round(alg_per_step / (min(kt) * 1e-3) / 1e9, 1),
+                                          "worst": round(alg_per_step / (max(kt) * 1e-3) / 1e9, 1),
+                                          "paper_mean_of_3": round(alg_per_step / (statistics.mean(kt[:3]) * 1e-3)
+                                                                   / 1e9, 1),
+                                          "passes": len(kt)}},
             "e2e": e2e,
             "cpu_baseline": cpu_baseline,
             "gpu_launches": launches,
