@@ -852,7 +852,10 @@ __global__ void nf4_gemm_reduce_kernel(const float* __restrict__ partial, int sp
 // With the 32 KB byte-pair table: BN 16: 24 KB x 6;  BN 32: 32 KB x 5;
 //   BN 64: 24 KB (2 chunks) x 6;  BN 128: 40 KB (2 chunks) x 4;  BN 256: 36 KB
 //   (1 chunk) x 5 (one accumulator: 256 + 3*32 TMEM columns).
-constexpr int kGroups = 3;
+#ifndef NF4_GEMM_GROUPS
+#define NF4_GEMM_GROUPS 3
+#endif
+constexpr int kGroups = NF4_GEMM_GROUPS;
 // (macros: tuning experiments only, tools/)
 #ifndef NF4_GEMM_CST_SMALL
 #define NF4_GEMM_CST_SMALL 6
