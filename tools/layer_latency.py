@@ -48,7 +48,7 @@ def main():
     with torch.cuda.graph(g, stream=s):
         batched()
 
-    def time_it(fn, cold):
+    def time_it(fn, cold, mean=False):
         ts = []
         for r in range(args.reps + 3):
             with torch.cuda.stream(s):
@@ -61,7 +61,7 @@ def main():
             s.synchronize()
             if r >= 3:
                 ts.append(a.elapsed_time(b) * 1e3)
-        return statistics.median(ts)
+        return statistics.mean(ts) if mean else statistics.median(ts)
 
     alg = ws.algorithmic_bytes()
     res = {"model": args.model, "tensors": len(tensors), "elements": ws.n_total, "algorithmic_bytes": alg}
@@ -70,6 +70,19 @@ def main():
             us = time_it(fn, cold)
             res[f"{name}_{'cold' if cold else 'hot'}_us"] = round(us, 1)
             res[f"{name}_{'cold' if cold else 'hot'}_gbs"] = round(alg / (us * 1e-6) / 1e9, 1)
+    # each projection as its own tensor: one launch, cold.  Single
+    # cold launches are this short that the event timestamps' ~2 us granularity shows in
+    # every sample, so these are MEANS over the reps (medians land on multiples of 2.048 us).
+    per = []
+    for t, d, e in zip(tensors, descs, ws.entries):
+        nb = -(-e.n // 64)
+        tb = (e.n + 1) // 2 + 2 * e.n + nb + 4 * (-(-nb // 256))
+        us = time_it(lambda d=d: nf4.nf4_dequantize_batched([d], "bf16", stream=s), True, mean=True)
+        per.append({"tensor": t.name, "shape": [t.rows, t.cols], "elements": e.n, "cold_us_mean": round(us, 2),
+                    "cold_gbs": round(tb / (us * 1e-6) / 1e9, 1)})
+    res["per_tensor"] = per
+    # floor of this measurement: a trivial one-block kernel timed the same way
+    res["trivial_kernel_cold_us_mean"] = round(time_it(lambda: sink.zero_(), True, mean=True), 2)
     print(json.dumps(res))
 
 
