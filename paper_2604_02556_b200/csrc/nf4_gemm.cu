@@ -252,6 +252,9 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* m
 #ifndef NF4_GEMM_PAIR_MAXBN
 #define NF4_GEMM_PAIR_MAXBN 256
 #endif
+#ifndef NF4_GEMM_ST_SPLIT
+#define NF4_GEMM_ST_SPLIT 2   // tcgen05.st pieces per 32-weight chunk piece (0: one x16 after the wait; 2: x8; 4: x4)
+#endif
 #ifndef NF4_GEMM_PAIR_ROW
 #define NF4_GEMM_PAIR_ROW 128
 #endif
@@ -584,7 +587,31 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
                     asm("mov.b64 {%0, %1}, %2;" : "=f"(ch), "=f"(cl) : "l"(r));
                     w[4 * cc + jj] = pack2_rn<BF16>(ch, cl);
                   }
+#if NF4_GEMM_ST_SPLIT
+                  // store each piece of 16/SPLIT columns as soon as it is complete: its words die,
+                  // so more table loads stay in flight under the 72-register cap
+                  constexpr int kWords = 16 / NF4_GEMM_ST_SPLIT, kCc = kWords / 4;
+                  if (cc % kCc == kCc - 1) {
+                    if (q == 0 && cc == kCc - 1) {
+                      mbar_wait_parity(&a_free[g], aph ^ 1u);        // the MMA is done with our previous A tiles
+                      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    }
+                    const int w0 = (cc / kCc) * kWords;
+                    const uint32_t taddr = tmem + tlane + uint32_t(A0 + (g * SUB + q) * 32 + half * 16 + w0);
+                    if constexpr (kWords == 8)
+                      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                                   ::"r"(taddr), "r"(w[w0]), "r"(w[w0 + 1]), "r"(w[w0 + 2]), "r"(w[w0 + 3]),
+                                   "r"(w[w0 + 4]), "r"(w[w0 + 5]), "r"(w[w0 + 6]), "r"(w[w0 + 7]) : "memory");
+                    else
+                      asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};"
+                                   ::"r"(taddr), "r"(w[w0]), "r"(w[w0 + 1]), "r"(w[w0 + 2]), "r"(w[w0 + 3])
+                                   : "memory");
+                  }
+#endif
                 }
+#if NF4_GEMM_ST_SPLIT
+                continue;   // stored
+#endif
               } else {
 #pragma unroll
               for (int cc = 0; cc < 4; ++cc) {
