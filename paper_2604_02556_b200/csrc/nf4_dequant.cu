@@ -68,6 +68,7 @@ static const Variant kVariants[] = {
     {"v2u4c", 8, 4, false, false, false, true},      // 9
     {"v2u4xc", 8, 4, false, false, true, true},      // 10
     {"v2u4sxcd", 8, 4, false, true, true, true},     // 11: + double-buffered scale cache / CLC slots
+    {"v2u4sxcp", 8, 4, false, true, true, true},     // 12: v2u4sxc + byte-pair table (32 KB smem per CTA)
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 constexpr int kDefaultVariant = 8;   // v2u4sxc: best measured on B200 (profiles/r01_variants.md)
@@ -184,6 +185,31 @@ __device__ __forceinline__ void decode_group(const float* lut, const CodeVec<VEC
   }
 }
 
+// Byte-pair table (variant 12): entry b = (NF4[b >> 4], NF4[b & 15]), one copy per
+// half-warp lane (row b = 128 B = 16 copies), so a 64-bit lookup per code BYTE is
+// bank-conflict-free for any codes: per two elements one PRMT (byte extract), one
+// IMAD (row address), one LDS.64, one FMUL2 and one F2FP (same numbers as decode_group).
+constexpr int kPairRow = 128;
+constexpr int kPairBytes = 256 * kPairRow;
+template <int OUT, int VEC>
+__device__ __forceinline__ void decode_group_pair(uint32_t ptab_lane, const CodeVec<VEC>& q, float a,
+                                                  uint32_t (&w)[OutWords<OUT, VEC>::value]) {
+  const uint64_t aa = f32x2_splat(a);
+#pragma unroll
+  for (int i = 0; i < VEC / 4; ++i) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t byte = __byte_perm(q.w[i], 0u, 0x4440u + k);
+      uint64_t v, r;
+      asm("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(ptab_lane + byte * kPairRow));
+      asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(v), "l"(aa));   // fl32(NF4[idx] * a), both elements
+      float ph, pl;
+      asm("mov.b64 {%0, %1}, %2;" : "=f"(ph), "=f"(pl) : "l"(r));
+      put_pair<OUT, VEC>(w, 4 * i + k, ph, pl);
+    }
+  }
+}
+
 template <int NW>
 __device__ __forceinline__ void st_group(void* out, const uint32_t (&w)[NW]) {
 #pragma unroll
@@ -253,7 +279,7 @@ __device__ __forceinline__ int64_t clc_result(const uint4* result) {
 }
 
 template <int OUT, int VEC, int U, bool PERSIST, bool SSCALE, bool PRMT, bool CLC, bool DB = false,
-          int MAXB = NF4_MAX_BATCH, bool EARLY = false>
+          int MAXB = NF4_MAX_BATCH, bool EARLY = false, bool PAIR = false>
 __global__ void __launch_bounds__(kThreads) dequant_kernel(const __grid_constant__ BatchParamsT<MAXB> P) {
   constexpr int GROUP = 2 * VEC;                      // elements per thread-group
   constexpr int64_t TILE = int64_t(kThreads) * GROUP * U;
@@ -266,6 +292,16 @@ __global__ void __launch_bounds__(kThreads) dequant_kernel(const __grid_constant
   __shared__ __align__(16) uint4 clc_res[NBUF];
   __shared__ __align__(8) uint64_t clc_bar[NBUF];
   if (threadIdx.x < 16) lut[threadIdx.x] = P.lut[threadIdx.x];  // kernel-parameter (constant) bank -> smem
+  extern __shared__ __align__(128) uint8_t ptab[];                // PAIR: kPairBytes of dynamic smem
+  if constexpr (PAIR) {
+    for (int i = threadIdx.x; i < 256 * (kPairRow / 16); i += kThreads) {
+      const int b = i / (kPairRow / 16);
+      const float h = P.lut[b >> 4], l = P.lut[b & 15];
+      *reinterpret_cast<float4*>(ptab + 16 * i) = make_float4(h, l, h, l);
+    }
+  }
+  const uint32_t ptab_lane =
+      static_cast<uint32_t>(__cvta_generic_to_shared(ptab)) + (threadIdx.x & 15u) * 8u;
   if (CLC && threadIdx.x == 0) {
     for (int i = 0; i < NBUF; ++i)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
@@ -347,7 +383,10 @@ __global__ void __launch_bounds__(kThreads) dequant_kernel(const __grid_constant
         for (int u = 0; u < U; ++u) {
           const int64_t e0 = e_tile + int64_t(u * kThreads + threadIdx.x) * GROUP;
           uint32_t w[OutWords<OUT, VEC>::value];
-          decode_group<OUT, VEC, PRMT>(lut, q[u], a[u], w);
+          if constexpr (PAIR)
+            decode_group_pair<OUT, VEC>(ptab_lane, q[u], a[u], w);
+          else
+            decode_group<OUT, VEC, PRMT>(lut, q[u], a[u], w);
           st_group(out_at<OUT>(d.out, e0), w);
         }
       } else {
@@ -397,6 +436,7 @@ static KernelFn kernel_for(int v) {
     case 8: return dequant_kernel<OUT, 8, 4, false, true, true, true>;
     case 9: return dequant_kernel<OUT, 8, 4, false, false, false, true>;
     case 10: return dequant_kernel<OUT, 8, 4, false, false, true, true>;
+    case 12: return dequant_kernel<OUT, 8, 4, false, true, true, true, false, NF4_MAX_BATCH, false, true>;
     default: return dequant_kernel<OUT, 8, 4, false, true, true, true, true>;
   }
 }
@@ -421,11 +461,11 @@ static int64_t tile_elems(int v) { return int64_t(kThreads) * 2 * kVariants[v].v
 // Launch with programmatic stream serialization (PDL): the kernel executes
 // griddepcontrol.wait before its first global access.
 template <typename Kernel, typename Params>
-static void launch_pdl(Kernel k, int grid, cudaStream_t stream, const Params& P) {
+static void launch_pdl(Kernel k, int grid, cudaStream_t stream, const Params& P, size_t smem = 0) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(grid));
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -474,7 +514,7 @@ static int occupancy(int v, int out) {
   if (c == 0) {
     int occ = 0;
     const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &occ, reinterpret_cast<const void*>(kernel_of(out, v)), kThreads, 0);
+        &occ, reinterpret_cast<const void*>(kernel_of(out, v)), kThreads, v == 12 ? size_t(kPairBytes) : 0);
     c = (e == cudaSuccess && occ > 0) ? occ : 4;
   }
   return c;
@@ -545,7 +585,7 @@ static nf4_status launch_batch(const nf4_tensor* ts, int count, int out, const f
     else launch_small<16>(P, out, grid, stream);
   } else {
     KernelFn fn = kernel_of(out, v);
-    launch_pdl(fn, grid, stream, P);
+    launch_pdl(fn, grid, stream, P, v == 12 ? size_t(kPairBytes) : 0);
   }
   const cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) {
