@@ -11,7 +11,10 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-if not os.environ.get("NF4_LIB"):   # event traces / experiments need the diagnostics build
+_exps_arg = sys.argv[4] if len(sys.argv) > 4 else "0,1,2,4,6,7"
+if not os.environ.get("NF4_LIB") and _exps_arg != "0":
+    # pipeline-skipping experiments need the diagnostics build (itself ~2x slower: its
+    # numbers compare experiments with each other, not with the production library)
     from paper_2604_02556_b200 import _build
     os.environ["NF4_LIB"] = _build.build_variant("exp", {"NF4_GEMM_DIAG": 2})
 import torch
