@@ -44,7 +44,19 @@
 namespace nf4 {
 namespace gemm {
 
-constexpr int kProducerWarps = 8;          // per producer group: 2 threads per weight row (32 elements each)
+// Producer groups per token-tile width BN: up to NF4_GEMM_W4_MAXBN (decode-size
+// M), 6 groups of 4 warps (one thread per weight row, both halves of each chunk;
+// 2-chunk super-stages, 6 x 2 A tiles in TMEM): more, smaller hand-offs, so a
+// group that ran ahead waits less for the in-order MMA.  Wider tiles keep 3 groups
+// of 8 warps (2 threads per row), whose 4-chunk stages suit the heavier MMA/X side.
+#ifndef NF4_GEMM_W4_MAXBN
+#define NF4_GEMM_W4_MAXBN 16
+#endif
+#ifndef NF4_GEMM_GROUPS
+#define NF4_GEMM_GROUPS 3   // 8-warp groups
+#endif
+template <int BN> __host__ __device__ constexpr int wpg_for() { return BN <= NF4_GEMM_W4_MAXBN ? 4 : 8; }
+template <int BN> __host__ __device__ constexpr int groups_for() { return BN <= NF4_GEMM_W4_MAXBN ? 6 : NF4_GEMM_GROUPS; }
 constexpr int kCodeBytes = 32;              // packed bytes per row per k-chunk
 constexpr int kChunk = 64;          // k elements per stage (= one 128 B swizzle row in 16-bit)
 constexpr int kRowBytes = 128;
@@ -378,12 +390,13 @@ struct Scales {
 // Grouped GEMMs (MULTI): the segment's member selects the TMA descriptor,
 // scale pointers, code2 table and output.
 template <int BN, int G, int SUB, int CST, int NACC, bool BF16, bool MULTI>
-__global__ void __launch_bounds__(32 * (8 * G + 2), 1)
+__global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
     nf4_gemm_kernel(const __grid_constant__ GemmParams p, const __grid_constant__ CodeMapsT<MULTI ? kMaxMembers : 1> maps,
                     const __grid_constant__ CUtensorMap map_x) {
   constexpr int kMem = MULTI ? kMaxMembers : 1;   // members this instantiation serves
   static_assert(CST >= G, "a super-stage slot must not be two phases behind any group");
-  constexpr int kMmaWarp = 8 * G, kTmaWarp = 8 * G + 1;
+  constexpr int kProducerWarps = wpg_for<BN>();
+  constexpr int kMmaWarp = kProducerWarps * G, kTmaWarp = kProducerWarps * G + 1;
   constexpr int ACC = BN < 32 ? 32 : BN;
   constexpr int A0 = NACC * ACC;
   static_assert(A0 + G * SUB * 32 <= 512, "TMEM budget");
@@ -473,11 +486,11 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
   const uint32_t tmem = tmem_holder;
   if (NF4_TRACING && cta_lin == 0 && threadIdx.x == 0) p.trace[0] = gtimer();
 
-  if (warp < 8 * G) {
+  if (warp < kProducerWarps * G) {
     // ======================= producers (dequantize into TMEM) + epilogue =======================
-    const int g = warp >> 3, wl = warp & 7;
+    const int g = warp / kProducerWarps, wl = warp % kProducerWarps;
     const int t = 32 * (wl & 3) + lane;        // tile row = TMEM lane
-    const int half = wl >> 2;
+    const int half = kProducerWarps == 8 ? wl >> 2 : 0;   // 4-warp groups: each thread does both halves
     const int chunk_shift = p.bs_shift - 6;    // 64-element chunks per quantization block = 2^chunk_shift
     const uint32_t tlane = uint32_t(32 * (wl & 3)) << 16;
     const uint32_t lut_base = smem_u32(lut);   // low byte 0: PRMT splices a byte offset into it
@@ -569,98 +582,115 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
             const int i = j * SUB + q;
             if (!FULL && i >= nk) break;
             uint32_t w[16];
-            if (!NF4_EXP(2)) {
-              float a;
-              if constexpr (MODE == 0) {
-                a = __uint_as_float(sc.s[q]);
-              } else if constexpr (MODE == 1) {
-                // A4 (R7): fl32(fl32(code2[qabsmax] * absmax2) + offset), two roundings
-                const uint32_t qb = (sc.s[0] >> (8 * q)) & 0xFFu;
-                const float a2 = ((b0 + q) >> 8) == (b0 >> 8) ? sc.a2[0] : sc.a2[1];
-                a = __fadd_rn(__fmul_rn(c2[qb], a2), offset);
-              } else {
-                a = __fadd_rn(__fmul_rn(c2[sc.s[q]], sc.a2[q]), offset);
-              }
+            float a = 0.0f;
+            if constexpr (MODE == 0) {
+              a = __uint_as_float(sc.s[q]);
+            } else if constexpr (MODE == 1) {
+              // A4 (R7): fl32(fl32(code2[qabsmax] * absmax2) + offset), two roundings
+              const uint32_t qb = (sc.s[0] >> (8 * q)) & 0xFFu;
+              const float a2 = ((b0 + q) >> 8) == (b0 >> 8) ? sc.a2[0] : sc.a2[1];
+              a = __fadd_rn(__fmul_rn(c2[qb], a2), offset);
+            } else {
+              a = __fadd_rn(__fmul_rn(c2[sc.s[q]], sc.a2[q]), offset);
+            }
+            const uint64_t aa = f32x2_splat(a);
+            // 8-warp groups: this thread's half of the chunk; 4-warp groups: both halves
+#pragma unroll
+            for (int hh = half; hh < (kProducerWarps == 8 ? half + 1 : 2); ++hh) {
               const uint4 c0 = *reinterpret_cast<const uint4*>(smem_c + cs * kSuperCodeBytes +
-                                                               code_chunk_off<SUB>(t, 2 * q + half));
+                                                               code_chunk_off<SUB>(t, 2 * q + hh));
               // dequantize 32 weights: word jj = (element 2jj) | (element 2jj+1) << 16
               const uint32_t cw[4] = {c0.x, c0.y, c0.z, c0.w};
-              const uint64_t aa = f32x2_splat(a);
-              if constexpr (pair_for<BN>()) {
+              const bool first = q == 0 && hh == half;
+              if constexpr (pair_for<BN>() && NF4_GEMM_ST_SPLIT != 0) {
 #pragma unroll
                 for (int cc = 0; cc < 4; ++cc) {
+                  if (!NF4_EXP(2)) {
 #pragma unroll
-                  for (int jj = 0; jj < 4; ++jj) {
-                    // row of byte jj of the word, this lane's copy
-                    const uint32_t byte = __byte_perm(cw[cc], 0u, 0x4440u + jj);
-                    uint64_t v, r;
-                    asm("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(ptab_lane + byte * NF4_GEMM_PAIR_ROW));
-                    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(v), "l"(aa));   // fl32(NF4[idx] * a), both
-                    float ch, cl;
-                    asm("mov.b64 {%0, %1}, %2;" : "=f"(ch), "=f"(cl) : "l"(r));
-                    w[4 * cc + jj] = pack2_rn<BF16>(ch, cl);
+                    for (int jj = 0; jj < 4; ++jj) {
+                      // row of byte jj of the word, this lane's copy
+                      const uint32_t byte = __byte_perm(cw[cc], 0u, 0x4440u + jj);
+                      uint64_t v, r;
+                      asm("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(ptab_lane + byte * NF4_GEMM_PAIR_ROW));
+                      asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(v), "l"(aa));   // fl32(NF4[idx] * a), both
+                      float ch, cl;
+                      asm("mov.b64 {%0, %1}, %2;" : "=f"(ch), "=f"(cl) : "l"(r));
+                      w[4 * cc + jj] = pack2_rn<BF16>(ch, cl);
+                    }
                   }
-#if NF4_GEMM_ST_SPLIT
                   // store each piece of 16/SPLIT columns as soon as it is complete: its words die,
-                  // so more table loads stay in flight under the 72-register cap
-                  constexpr int kWords = 16 / NF4_GEMM_ST_SPLIT, kCc = kWords / 4;
+                  // so more table loads stay in flight under the 72-register cap.  The first
+                  // piece of a super-stage is dequantized before waiting for the MMA to release
+                  // the A tiles (a warp that ran ahead of its group keeps working).
+                  constexpr int kWords = 16 / (NF4_GEMM_ST_SPLIT ? NF4_GEMM_ST_SPLIT : 1), kCc = kWords / 4;
                   if (cc % kCc == kCc - 1) {
-                    if (q == 0 && cc == kCc - 1) {
+                    if (first && cc == kCc - 1) {
                       mbar_wait_parity(&a_free[g], aph ^ 1u);        // the MMA is done with our previous A tiles
+                      if (wl == 0 && lane == 0) NF4_TRACE_J(200, Jg);
                       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     }
                     const int w0 = (cc / kCc) * kWords;
-                    const uint32_t taddr = tmem + tlane + uint32_t(A0 + (g * SUB + q) * 32 + half * 16 + w0);
-                    if constexpr (kWords == 8)
-                      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
-                                   ::"r"(taddr), "r"(w[w0]), "r"(w[w0 + 1]), "r"(w[w0 + 2]), "r"(w[w0 + 3]),
-                                   "r"(w[w0 + 4]), "r"(w[w0 + 5]), "r"(w[w0 + 6]), "r"(w[w0 + 7]) : "memory");
-                    else
-                      asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};"
-                                   ::"r"(taddr), "r"(w[w0]), "r"(w[w0 + 1]), "r"(w[w0 + 2]), "r"(w[w0 + 3])
-                                   : "memory");
+                    const uint32_t taddr = tmem + tlane + uint32_t(A0 + (g * SUB + q) * 32 + hh * 16 + w0);
+                    if (!NF4_EXP(4)) {
+                      if constexpr (kWords == 8)
+                        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                                     ::"r"(taddr), "r"(w[w0]), "r"(w[w0 + 1]), "r"(w[w0 + 2]), "r"(w[w0 + 3]),
+                                     "r"(w[w0 + 4]), "r"(w[w0 + 5]), "r"(w[w0 + 6]), "r"(w[w0 + 7]) : "memory");
+                      else
+                        asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};"
+                                     ::"r"(taddr), "r"(w[w0]), "r"(w[w0 + 1]), "r"(w[w0 + 2]), "r"(w[w0 + 3])
+                                     : "memory");
+                    }
                   }
-#endif
                 }
-#if NF4_GEMM_ST_SPLIT
-                continue;   // stored
-#endif
               } else {
+                if (!NF4_EXP(2)) {
 #pragma unroll
-              for (int cc = 0; cc < 4; ++cc) {
-                const uint32_t x = cw[cc];
-                const uint32_t hi4 = (x >> 2) & 0x3C3C3C3Cu;  // byte jj = 4 * high nibble (LUT byte offset)
-                const uint32_t lo4 = (x << 2) & 0x3C3C3C3Cu;  // byte jj = 4 * low nibble
+                  for (int cc = 0; cc < 4; ++cc) {
+                    if constexpr (pair_for<BN>()) {
 #pragma unroll
-                for (int jj = 0; jj < 4; ++jj) {
-                  // shared address of NF4[idx] = lut_base with byte 0 replaced by byte jj of hi4/lo4: one PRMT
-                  const uint32_t ah = __byte_perm(hi4, lut_base, 0x7650u + jj);
-                  const uint32_t al = __byte_perm(lo4, lut_base, 0x7650u + jj);
-                  float ch, cl;
-                  asm("ld.shared.f32 %0, [%1];" : "=f"(ch) : "r"(ah));
-                  asm("ld.shared.f32 %0, [%1];" : "=f"(cl) : "r"(al));
-                  mul2_rn(ch, cl, aa);                      // fl32(NF4[idx] * a) for both, one FMUL2
-                  w[4 * cc + jj] = pack2_rn<BF16>(ch, cl);
+                      for (int jj = 0; jj < 4; ++jj) {
+                        const uint32_t byte = __byte_perm(cw[cc], 0u, 0x4440u + jj);
+                        uint64_t v, r;
+                        asm("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(ptab_lane + byte * NF4_GEMM_PAIR_ROW));
+                        asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(v), "l"(aa));
+                        float ch, cl;
+                        asm("mov.b64 {%0, %1}, %2;" : "=f"(ch), "=f"(cl) : "l"(r));
+                        w[4 * cc + jj] = pack2_rn<BF16>(ch, cl);
+                      }
+                    } else {
+                      const uint32_t x = cw[cc];
+                      const uint32_t hi4 = (x >> 2) & 0x3C3C3C3Cu;  // byte jj = 4 * high nibble (LUT byte offset)
+                      const uint32_t lo4 = (x << 2) & 0x3C3C3C3Cu;  // byte jj = 4 * low nibble
+#pragma unroll
+                      for (int jj = 0; jj < 4; ++jj) {
+                        // shared address of NF4[idx] = lut_base with byte 0 replaced by byte jj of hi4/lo4: one PRMT
+                        const uint32_t ah = __byte_perm(hi4, lut_base, 0x7650u + jj);
+                        const uint32_t al = __byte_perm(lo4, lut_base, 0x7650u + jj);
+                        float ch, cl;
+                        asm("ld.shared.f32 %0, [%1];" : "=f"(ch) : "r"(ah));
+                        asm("ld.shared.f32 %0, [%1];" : "=f"(cl) : "r"(al));
+                        mul2_rn(ch, cl, aa);                      // fl32(NF4[idx] * a) for both, one FMUL2
+                        w[4 * cc + jj] = pack2_rn<BF16>(ch, cl);
+                      }
+                    }
+                  }
+                }
+                if (first) {
+                  mbar_wait_parity(&a_free[g], aph ^ 1u);              // the MMA is done with our previous A tiles
+                  if (wl == 0 && lane == 0) NF4_TRACE_J(200, Jg);
+                  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                }
+                if (!NF4_EXP(4)) {
+                  // 16 columns (32 weights) of this row's A tile (group g, chunk q) in TMEM
+                  const uint32_t taddr = tmem + tlane + uint32_t(A0 + (g * SUB + q) * 32 + hh * 16);
+                  asm volatile(
+                      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+                      ::"r"(taddr), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]),
+                      "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]), "r"(w[15])
+                      : "memory");
                 }
               }
-              }
-            }
-            if (q == 0) {
-              // The first chunk is dequantized into registers before this wait, so a
-              // warp that finished its previous super-stage ahead of the rest of its
-              // group (and of the MMA that must release the A tiles) keeps working.
-              mbar_wait_parity(&a_free[g], aph ^ 1u);                // the MMA is done with our previous A tiles
-              if (wl == 0 && lane == 0) NF4_TRACE_J(200, Jg);
-              asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            }
-            if (!NF4_EXP(4)) {
-              // 16 columns (32 weights) of this row's A tile (group g, chunk q) in TMEM
-              const uint32_t taddr = tmem + tlane + uint32_t(A0 + (g * SUB + q) * 32 + half * 16);
-              asm volatile(
-                  "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
-                  ::"r"(taddr), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]),
-                  "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]), "r"(w[15])
-                  : "memory");
             }
           }
         };
@@ -689,7 +719,8 @@ __global__ void __launch_bounds__(32 * (8 * G + 2), 1)
         asm volatile("griddepcontrol.wait;" ::: "memory");   // y / partials / counters: the previous kernel is done
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const int qd = wl & 3;                           // TMEM lane quarter this warp may access
-        constexpr int HB = BN / 2 < 16 ? 16 : BN / 2;    // columns per warp (BN = 16: warps 4-7 idle)
+        // columns per warp (8-warp groups, BN = 16: warps 4-7 idle; 4-warp groups: all BN)
+        constexpr int HB = kProducerWarps == 4 ? BN : (BN / 2 < 16 ? 16 : BN / 2);
         const int col0 = half * HB;
         const int n = sg.n0 + qd * 32 + lane;
         const uint32_t taddr = tmem + (uint32_t(qd * 32) << 16) + uint32_t(ab * ACC);
@@ -892,10 +923,6 @@ __global__ void nf4_gemm_reduce_kernel(const float* __restrict__ partial, int sp
 // With the 32 KB byte-pair table: BN 16: 24 KB x 6;  BN 32: 32 KB x 5;
 //   BN 64: 24 KB (2 chunks) x 6;  BN 128: 40 KB (2 chunks) x 4;  BN 256: 36 KB
 //   (1 chunk) x 5 (one accumulator: 256 + 3*32 TMEM columns).
-#ifndef NF4_GEMM_GROUPS
-#define NF4_GEMM_GROUPS 3
-#endif
-constexpr int kGroups = NF4_GEMM_GROUPS;
 // (macros: tuning experiments only, tools/)
 #ifndef NF4_GEMM_CST_SMALL
 #define NF4_GEMM_CST_SMALL 6
@@ -925,9 +952,11 @@ constexpr int kGroups = NF4_GEMM_GROUPS;
 #define NF4_GEMM_PCST128 4
 #endif
 template <int BN> constexpr int sub_for() {
+  if (wpg_for<BN>() == 4) return BN <= 64 ? 2 : 1;   // 6 groups of 4 warps: TMEM holds 6 x SUB A tiles
   return BN <= 16 ? 4 : BN <= 32 ? NF4_GEMM_SUB32 : BN <= 64 ? NF4_GEMM_SUB64 : BN <= 128 ? NF4_GEMM_SUB128 : 1;
 }
 template <int BN> constexpr int cst_for() {
+  if (wpg_for<BN>() == 4) return BN <= 32 ? 8 : 6;
   // with the 32 KB pair table: 6 / 5 / 6 (2-chunk) / 4 / 5 stages fit in 227 KB (64 KB table: 6 / 4 / 3 / 3 / 4)
   return pair_for<BN>() ? (NF4_GEMM_PAIR_ROW == 128
                                ? (BN <= 16 ? NF4_GEMM_CST_SMALL : BN <= 32 ? NF4_GEMM_PCST32 : BN <= 64 ? NF4_GEMM_PCST64
@@ -941,7 +970,7 @@ static int sub_of(int bn) {
                                                                                             : sub_for<256>();
 }
 template <int BN> constexpr int nacc_for() { return BN <= 128 ? 2 : 1; }
-constexpr int threads_for() { return 32 * (8 * kGroups + 2); }
+template <int BN> constexpr int threads_for() { return 32 * (wpg_for<BN>() * groups_for<BN>() + 2); }
 
 template <int BN>
 constexpr size_t smem_bytes() {
@@ -950,7 +979,7 @@ constexpr size_t smem_bytes() {
 
 template <int BN, bool BF16, bool MULTI>
 constexpr auto kernel_for() {
-  return nf4_gemm_kernel<BN, kGroups, sub_for<BN>(), cst_for<BN>(), nacc_for<BN>(), BF16, MULTI>;
+  return nf4_gemm_kernel<BN, groups_for<BN>(), sub_for<BN>(), cst_for<BN>(), nacc_for<BN>(), BF16, MULTI>;
 }
 
 template <int BN, bool BF16, bool MULTI>
@@ -968,7 +997,7 @@ static cudaError_t launch1(const GemmParams& p, const CodeMaps& mc, const CUtens
   // griddepcontrol.wait before reading any input)
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
-  cfg.blockDim = dim3(threads_for());
+  cfg.blockDim = dim3(threads_for<BN>());
   cfg.dynamicSmemBytes = sm;
   cfg.stream = s;
   cudaLaunchAttribute at[1];

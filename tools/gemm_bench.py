@@ -39,6 +39,7 @@ def main():
     ap.add_argument("--splits", type=int, default=0,
                     help="0: stream-K (default); -1: classic grid, makespan split heuristic; >0: classic, fixed")
     ap.add_argument("--no-unfused", action="store_true")
+    ap.add_argument("--graph", action="store_true", help="replay each step from a CUDA graph")
     ap.add_argument("--grouped", action="store_true",
                     help="q/k/v and gate/up of each layer as one nf4_gemm_grouped launch (they share X)")
     args = ap.parse_args()
@@ -120,14 +121,26 @@ def main():
                 members = [(ws._ptr(ws.codes, ws.entries[i].codes_off), None, dqs[i], tensors[i].rows) for i in grp]
                 nf4.nf4_gemm_grouped(xs[K], members, K=K, ys=[ys[i] for i in grp], workspace=gws[tuple(grp)])
 
-    fused_ms = timeit(grouped_step if args.grouped else fused_step)
+    step = grouped_step if args.grouped else fused_step
+    if args.graph:
+        # the whole step as one CUDA graph (no host launch overhead; PDL edges kept)
+        gs = torch.cuda.Stream()
+        gs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(gs):
+            step()
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=gs):
+            step()
+        step = graph.replay
+    fused_ms = timeit(step)
     n_total = sum(t.n for t in tensors)
     bytes_w = sum((e.n // 2) + (e.n // 64) + 4 * (e.n // 64 // 256) for e in ws.entries)
     bytes_xy = sum(M * t.cols * 2 + M * t.rows * 2 for t in tensors)
     flops = 2.0 * M * n_total
     res = {"model": args.model, "layers": args.layers or wl.MODELS[args.model][0], "M": M,
            "tensors": len(tensors), "weight_elements": n_total,
-           "fused_ms": round(fused_ms, 4),
+           "fused_ms": round(fused_ms, 4), "graph": bool(args.graph),
            "fused_hbm_gbs": round((bytes_w + bytes_xy) / (fused_ms * 1e-3) / 1e9, 1),
            "fused_tflops": round(flops / (fused_ms * 1e-3) / 1e12, 2),
            # roofline of the fused kernel: one shared-memory LUT lookup per weight,
