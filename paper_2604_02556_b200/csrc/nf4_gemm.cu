@@ -45,8 +45,8 @@ namespace nf4 {
 namespace gemm {
 
 // Producer groups per token-tile width BN: up to NF4_GEMM_W4_MAXBN (decode-size
-// M), 6 groups of 4 warps (one thread per weight row, both halves of each chunk;
-// 2-chunk super-stages, 6 x 2 A tiles in TMEM): more, smaller hand-offs, so a
+// M), 5 groups of 4 warps (one thread per weight row, both halves of each chunk;
+// 2-chunk super-stages x 10, 5 x 2 A tiles in TMEM): more, smaller hand-offs, so a
 // group that ran ahead waits less for the in-order MMA.  Wider tiles keep 3 groups
 // of 8 warps (2 threads per row), whose 4-chunk stages suit the heavier MMA/X side.
 #ifndef NF4_GEMM_W4_MAXBN
@@ -55,8 +55,14 @@ namespace gemm {
 #ifndef NF4_GEMM_GROUPS
 #define NF4_GEMM_GROUPS 3   // 8-warp groups
 #endif
+#ifndef NF4_GEMM_W4_GROUPS
+#define NF4_GEMM_W4_GROUPS 5
+#endif
+#ifndef NF4_GEMM_W4_CST
+#define NF4_GEMM_W4_CST 10
+#endif
 template <int BN> __host__ __device__ constexpr int wpg_for() { return BN <= NF4_GEMM_W4_MAXBN ? 4 : 8; }
-template <int BN> __host__ __device__ constexpr int groups_for() { return BN <= NF4_GEMM_W4_MAXBN ? 6 : NF4_GEMM_GROUPS; }
+template <int BN> __host__ __device__ constexpr int groups_for() { return BN <= NF4_GEMM_W4_MAXBN ? NF4_GEMM_W4_GROUPS : NF4_GEMM_GROUPS; }
 constexpr int kCodeBytes = 32;              // packed bytes per row per k-chunk
 constexpr int kChunk = 64;          // k elements per stage (= one 128 B swizzle row in 16-bit)
 constexpr int kRowBytes = 128;
@@ -956,7 +962,7 @@ template <int BN> constexpr int sub_for() {
   return BN <= 16 ? 4 : BN <= 32 ? NF4_GEMM_SUB32 : BN <= 64 ? NF4_GEMM_SUB64 : BN <= 128 ? NF4_GEMM_SUB128 : 1;
 }
 template <int BN> constexpr int cst_for() {
-  if (wpg_for<BN>() == 4) return BN <= 32 ? 8 : 6;
+  if (wpg_for<BN>() == 4) return BN <= 32 ? NF4_GEMM_W4_CST : 6;
   // with the 32 KB pair table: 6 / 5 / 6 (2-chunk) / 4 / 5 stages fit in 227 KB (64 KB table: 6 / 4 / 3 / 3 / 4)
   return pair_for<BN>() ? (NF4_GEMM_PAIR_ROW == 128
                                ? (BN <= 16 ? NF4_GEMM_CST_SMALL : BN <= 32 ? NF4_GEMM_PCST32 : BN <= 64 ? NF4_GEMM_PCST64
