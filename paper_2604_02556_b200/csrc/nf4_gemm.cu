@@ -995,6 +995,10 @@ static cudaError_t launch1(const GemmParams& p, const CodeMaps& mc, const CUtens
   CodeMapsT<MULTI ? kMaxMembers : 1> maps;
   memcpy(&maps, &mc, sizeof(maps));
   constexpr size_t sm = smem_bytes<BN>();
+  // 227 KB per block, minus the static shared memory (LUT, code2 tables, barriers: < 6 KB)
+  static_assert(sm + 6 * 1024 <= 232448, "shared-memory budget (stages + pair table) exceeded");
+  static_assert(nacc_for<BN>() * (BN < 32 ? 32 : BN) + groups_for<BN>() * sub_for<BN>() * 32 <= 512, "TMEM budget");
+  static_assert(cst_for<BN>() >= groups_for<BN>(), "a super-stage slot must not be two phases behind any group");
   static std::once_flag once;          // per instantiation (per process: one device type)
   static cudaError_t attr = cudaSuccess;
   std::call_once(once, [&] { attr = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)); });
