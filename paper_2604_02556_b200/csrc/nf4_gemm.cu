@@ -49,6 +49,11 @@ namespace gemm {
 // 2-chunk super-stages x 10, 5 x 2 A tiles in TMEM): more, smaller hand-offs, so a
 // group that ran ahead waits less for the in-order MMA.  Wider tiles keep 3 groups
 // of 8 warps (2 threads per row), whose 4-chunk stages suit the heavier MMA/X side.
+// DQ second-level table: read through L1 from global memory (no prologue staging,
+// whose global round trip sat before the block-wide sync) instead of from smem.
+#ifndef NF4_GEMM_CODE2_GLOBAL
+#define NF4_GEMM_CODE2_GLOBAL 1   // 1: -4% at M=1, -1% at M=128 (grouped 8-layer step)
+#endif
 #ifndef NF4_GEMM_W4_MAXBN
 #define NF4_GEMM_W4_MAXBN 16
 #endif
@@ -410,7 +415,7 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
   constexpr int kSuperXBytes = SUB * BN * kRowBytes;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ __align__(256) float lut[16];                    // 256-B aligned: address = PRMT(offsets, base)
-  __shared__ float code2s[kMem][256];                         // DQ second-level tables
+  __shared__ float code2s[kMem][NF4_GEMM_CODE2_GLOBAL ? 1 : 256];   // DQ second-level tables (staged variant)
   __shared__ __align__(8) uint64_t c_full[CST], x_full[CST], c_free[CST], w_full[G], a_free[G], acc_full[NACC],
       acc_empty[NACC];
   __shared__ uint32_t tmem_holder;
@@ -484,7 +489,8 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
   if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   for (int i = 0; i < kMem && i < p.nmem; ++i) {
     if (p.mem[i].absmax == nullptr)
-      for (int t = threadIdx.x; t < 256; t += blockDim.x) code2s[i][t] = p.mem[i].code2[t];
+      if (!NF4_GEMM_CODE2_GLOBAL)
+        for (int t = threadIdx.x; t < 256; t += blockDim.x) code2s[i][t] = p.mem[i].code2[t];
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -512,7 +518,7 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
 #define qabsmax (p.mem[sg.g].qabsmax)
 #define absmax2 (p.mem[sg.g].absmax2)
       const float offset = p.mem[sg.g].offset;
-      const float* c2 = code2s[sg.g];
+      const float* c2 = NF4_GEMM_CODE2_GLOBAL ? p.mem[sg.g].code2 : code2s[sg.g];
       const int Nm = p.mem[sg.g].N;
       const int row = sg.n0 + t;
       const bool row_ok = row < Nm;
@@ -595,9 +601,9 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
               // A4 (R7): fl32(fl32(code2[qabsmax] * absmax2) + offset), two roundings
               const uint32_t qb = (sc.s[0] >> (8 * q)) & 0xFFu;
               const float a2 = ((b0 + q) >> 8) == (b0 >> 8) ? sc.a2[0] : sc.a2[1];
-              a = __fadd_rn(__fmul_rn(c2[qb], a2), offset);
+              a = __fadd_rn(__fmul_rn(NF4_GEMM_CODE2_GLOBAL ? __ldg(c2 + qb) : c2[qb], a2), offset);
             } else {
-              a = __fadd_rn(__fmul_rn(c2[sc.s[q]], sc.a2[q]), offset);
+              a = __fadd_rn(__fmul_rn(NF4_GEMM_CODE2_GLOBAL ? __ldg(c2 + sc.s[q]) : c2[sc.s[q]], sc.a2[q]), offset);
             }
             const uint64_t aa = f32x2_splat(a);
             // 8-warp groups: this thread's half of the chunk; 4-warp groups: both halves
