@@ -456,6 +456,59 @@ def test_double_quantize_bruteforce(orc):
     assert np.max(np.abs(dec - absmax) / np.abs(absmax)) < 0.05
 
 
+def dq_tie_fixture():
+    """Blocks whose normalized second-level value dn sits EXACTLY midway between
+    two adjacent code2 entries (fl32|dn - c_i| == fl32|dn - c_i+1|), so the
+    tie rule alone decides q.  Group 0: offset 0, one block at absmax 1.0 makes
+    s2 = 1 and dn = absmax exactly; group 1 (second call) uses offset 1.0 and a
+    block at 2.0 (d = +1) so d = absmax - 1 reaches the negative midpoints.
+    Returns [(absmax fp32[256], offset, expected q per tie block {block: i})]."""
+    code2 = syn.dynamic_map_code2()
+    ties = []
+    for i in range(255):
+        m = (np.float64(code2[i]) + np.float64(code2[i + 1])) / 2
+        if np.float64(np.float32(m)) != m:
+            continue
+        m32 = np.float32(m)
+        if abs(np.float32(m32 - code2[i])) == abs(np.float32(m32 - code2[i + 1])):
+            ties.append((i, m32))
+    assert len(ties) > 100
+    out = []
+    # non-negative midpoints, offset 0
+    pos = [(i, m) for i, m in ties if m >= 0][:200]
+    a = np.full(256, 0.5, np.float32)
+    a[0] = 1.0
+    exp = {}
+    for j, (i, m) in enumerate(pos[:255]):
+        a[1 + j] = m
+        exp[1 + j] = i
+    out.append((a, 0.0, exp))
+    # negative midpoints through offset 1.0: absmax = 1 + m must give d = m exactly
+    neg = [(i, m) for i, m in ties if m < 0 and np.float32(np.float32(1.0 + m) - np.float32(1.0)) == m]
+    a = np.full(256, 1.0, np.float32)
+    a[0] = 2.0
+    exp = {}
+    for j, (i, m) in enumerate(neg[:255]):
+        a[1 + j] = np.float32(1.0 + m)
+        exp[1 + j] = i
+    assert len(exp) > 20
+    out.append((a, 1.0, exp))
+    return code2, out
+
+
+def test_double_quantize_ties_go_to_lower_index(orc):
+    """SPEC S:98 / S:129 (nearest code, ties broken toward the smaller index;
+    SURVEY 8(c) item 19): every exact tie must choose the LOWER code2 index.
+    Expected indices come from the fixture's construction (i, not i + 1), not
+    from any implementation."""
+    code2, cases = dq_tie_fixture()
+    for absmax, off, exp in cases:
+        q, a2 = orc.double_quantize(absmax, off, code2, 256)
+        assert a2[0] == 1.0
+        for b, i in exp.items():
+            assert q[b] == i, (b, i, int(q[b]), float(absmax[b]))
+
+
 def test_double_quantize_zero_group(orc):
     code2 = syn.dynamic_map_code2()
     absmax = np.full(300, 0.25, np.float32)

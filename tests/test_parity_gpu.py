@@ -259,6 +259,22 @@ def test_double_quantize_parity(nf4, orc):
         torch.cuda.synchronize()
         assert np.array_equal(d.qabsmax.cpu().numpy(), rq)
         assert np.array_equal(d.absmax2.cpu().numpy(), ra2)
+    # exact ties between adjacent code2 entries go to the lower index
+    from tests.test_oracle_pins import dq_tie_fixture
+    c2, cases = dq_tie_fixture()
+    for absmax, off, exp in cases:
+        rq, _ = orc.double_quantize(absmax, off, c2)
+        d = nf4.nf4_double_quantize(dev(absmax), off, dev(c2))
+        torch.cuda.synchronize()
+        got = d.qabsmax.cpu().numpy()
+        assert np.array_equal(got, rq)
+        assert all(got[b] == i for b, i in exp.items())
+        # the brute-force (unsorted-table) path takes the same tie decision
+        perm = np.arange(256)[::-1].copy()
+        d = nf4.nf4_double_quantize(dev(absmax), off, dev(c2[perm]))
+        rq2, _ = orc.double_quantize(absmax, off, c2[perm])
+        torch.cuda.synchronize()
+        assert np.array_equal(d.qabsmax.cpu().numpy(), rq2)
     # unsorted code2 takes the brute-force path
     perm = np.random.Generator(np.random.Philox(3)).permutation(256)
     c2u = code2[perm]
