@@ -279,3 +279,149 @@ def test_gemm_argument_errors(nf4):
     with pytest.raises(nf4.NF4Error) as e:
         nf4.nf4_gemm(x, p, a, None, N=128, K=100)             # K not a multiple of 64
     assert e.value.status == 2
+
+
+# ---------------------------------------------------------------------------
+# every weight bit-exact, and exact sums (verdict r01: the one-hot test read only
+# M of the K columns; the random-X bound admits one mis-decoded weight)
+# ---------------------------------------------------------------------------
+def _x_tensor(x16, xdt, M, K):
+    import torch
+    tdt = torch.bfloat16 if xdt == "bf16" else torch.float16
+    return dev(x16.view(np.int16)).view(tdt).reshape(M, K)
+
+
+def _to16(xf, xdt):
+    return (xf.astype(ml_dtypes.bfloat16) if xdt == "bf16" else xf.astype(np.float16)).view(np.uint16)
+
+
+def _pos0(a):
+    """fp32 values with -0 folded into +0 (a one-hot sum's zero sign depends on
+    the order of the zero terms, not on the weight)."""
+    a = np.asarray(a, np.float32) + np.float32(0.0)
+    return a.view(np.uint32)
+
+
+FULL_CASES = [  # (M -> token-tile width BN, N, K, blocksize)
+    (1, 256, 512, 64), (16, 2688, 5376, 64), (32, 640, 2048, 128), (64, 384, 1024, 64), (128, 200, 1024, 256)]
+
+
+@pytest.mark.parametrize("xdt", ["bf16", "f16"])
+@pytest.mark.parametrize("dq", [False, True])
+def test_gemm_recovers_every_weight_bit_exact(nf4, orc, xdt, dq):
+    """X = identity blocks covering all of K, one stream-K GEMM per block of M
+    columns: Y[m, n] = W[n, k0 + m] exactly, so EVERY dequantized weight the
+    tensor cores consumed is compared with the oracle's, at every token-tile
+    width (BN 16 / 32 / 64 / 128) and several blocksizes."""
+    import torch
+    code = orc.OUT_BF16 if xdt == "bf16" else orc.OUT_F16
+    np16 = ml_dtypes.bfloat16 if xdt == "bf16" else np.float16
+    for (M, N, K, bs) in FULL_CASES:
+        packed, kw = _weights(N, K, bs, dq, seed=7 * M + N + K + int(dq))
+        pk = dev(packed)
+        if dq:
+            absmax, d = None, nf4.DQ(dev(kw["qabsmax"]), dev(kw["code2"]), dev(kw["absmax2"]), kw["offset"])
+        else:
+            absmax, d = dev(kw["absmax"]), None
+        ws = torch.zeros(max(16, nf4.nf4_gemm_workspace_bytes(M, N, K, 0)), dtype=torch.uint8, device="cuda")
+        w_gpu = np.zeros((N, K), np.float32)
+        for k0 in range(0, K, M):
+            x = np.zeros((M, K), np.float32)
+            x[np.arange(M), k0 + np.arange(M)] = 1.0
+            y = nf4.nf4_gemm(_x_tensor(_to16(x, xdt), xdt, M, K), pk, absmax, d, N=N, K=K, blocksize=bs,
+                             y_dtype="f32", workspace=ws)
+            torch.cuda.synchronize()
+            w_gpu[:, k0:k0 + M] = y.cpu().numpy().T
+        want = orc.dequantize(packed, N * K, bs, code, threads=8, **kw).view(np16).astype(np.float32).reshape(N, K)
+        bad = _pos0(w_gpu) != _pos0(want)
+        assert not bad.any(), (M, N, K, bs, int(bad.sum()), np.argwhere(bad)[:3].tolist())
+
+
+def _sparse_pm1(M, K, nnz, seed):
+    """X rows with `nnz` entries of +-1 at random columns (rest 0)."""
+    rng = np.random.Generator(np.random.Philox(seed))
+    x = np.zeros((M, K), np.float32)
+    for m in range(M):
+        cols = rng.choice(K, nnz, replace=False)
+        x[m, cols] = rng.choice(np.array([-1.0, 1.0], np.float32), nnz)
+    return x
+
+
+def _exact_reference(x16, xdt, packed, N, K, bs, kw, orc):
+    """Y in fp64 from the oracle's weights; with +-1 X and few non-zeros every
+    partial sum is a multiple of the weights' smallest ulp and below 2^24 of
+    them, so ANY fp32 summation order gives exactly this value (checked here)."""
+    code = orc.OUT_BF16 if xdt == "bf16" else orc.OUT_F16
+    ref, mag = orc.gemm_reference(x16, code, packed, N, K, bs, **kw)
+    np16 = ml_dtypes.bfloat16 if xdt == "bf16" else np.float16
+    w = orc.dequantize(packed, N * K, bs, code, threads=8, **kw).view(np16).astype(np.float64)
+    nz = np.abs(w[w != 0])
+    _, e = np.frexp(nz)                              # nz = f * 2^e, f in [0.5, 1)
+    mant = 8 if xdt == "bf16" else 11
+    ulp = np.ldexp(1.0, int(e.min()) - mant)
+    assert mag.max() < ulp * 2.0 ** 24, "fixture: sums not exact in fp32"
+    assert np.array_equal(ref.astype(np.float32).astype(np.float64), ref)
+    return ref
+
+
+@pytest.mark.parametrize("xdt", ["bf16", "f16"])
+@pytest.mark.parametrize("dq", [False, True])
+def test_gemm_sparse_pm1_exact(nf4, orc, xdt, dq):
+    """X with 64 entries of +-1 per row: the exact Y is representable in fp32 and
+    reached by every summation order, so stream-K Y must equal the fp64 oracle
+    product BIT FOR BIT (fp32 output), and its RNE to bf16 / fp16 (16-bit output).
+    A single mis-decoded weight, a dropped k-chunk or a wrong partial changes Y."""
+    for (M, N, K, bs) in [(1, 512, 1024, 64), (16, 2688, 5376, 64), (40, 640, 2048, 128), (100, 384, 1024, 64),
+                          (128, 256, 3072, 64), (200, 384, 1024, 256)]:
+        packed, kw = _weights(N, K, bs, dq, seed=3 * M + N + K + int(dq))
+        x16 = _to16(_sparse_pm1(M, K, 64, M + K), xdt)
+        ref = _exact_reference(x16, xdt, packed, N, K, bs, kw, orc)
+        y = _run(nf4, x16, xdt, M, packed, kw, N, K, bs, "f32", 0).cpu().numpy()
+        assert np.array_equal(_pos0(y), _pos0(ref.astype(np.float32))), (M, N, K, bs)
+        y16 = _run(nf4, x16, xdt, M, packed, kw, N, K, bs, xdt, 0)
+        got = y16.view(__import__("torch").int16).cpu().numpy().view(np.uint16)
+        want = _to16(ref.astype(np.float32), xdt)
+        np16 = ml_dtypes.bfloat16 if xdt == "bf16" else np.float16
+        assert np.array_equal(_pos0(got.view(np16).astype(np.float32)), _pos0(want.view(np16).astype(np.float32))), \
+            (M, N, K, bs)
+
+
+@pytest.mark.parametrize("M", [1, 16, 64])
+def test_gemm_grouped_sparse_pm1_exact_and_full_weights(nf4, orc, M):
+    """nf4_gemm_grouped: exact sums (sparse +-1 X) for every member, and every
+    weight of every member recovered through identity X blocks."""
+    import torch
+    K = 1024
+    Ns = (512, 200, 384, 128)
+    dqs = (True, False, True, False)
+    members, kws, packs = [], [], []
+    for i, (N, dq) in enumerate(zip(Ns, dqs)):
+        packed, kw = _weights(N, K, 64, dq, seed=700 + i + M)
+        packs.append(packed)
+        kws.append(kw)
+        if dq:
+            members.append((dev(packed), None, nf4.DQ(dev(kw["qabsmax"]), dev(kw["code2"]), dev(kw["absmax2"]),
+                                                      kw["offset"]), N))
+        else:
+            members.append((dev(packed), dev(kw["absmax"]), None, N))
+    x16 = _to16(_sparse_pm1(M, K, 64, 5 + M), "bf16")
+    ys = nf4.nf4_gemm_grouped(_x_tensor(x16, "bf16", M, K), members, K=K, y_dtype="f32")
+    torch.cuda.synchronize()
+    for i, N in enumerate(Ns):
+        ref = _exact_reference(x16, "bf16", packs[i], N, K, 64, kws[i], orc)
+        assert np.array_equal(_pos0(ys[i].cpu().numpy()), _pos0(ref.astype(np.float32))), (M, i)
+    ws = torch.zeros(max(16, nf4.nf4_gemm_grouped_workspace_bytes(M, Ns, K)), dtype=torch.uint8, device="cuda")
+    w_gpu = [np.zeros((N, K), np.float32) for N in Ns]
+    for k0 in range(0, K, M):
+        m_eff = min(M, K - k0)
+        x = np.zeros((M, K), np.float32)
+        x[np.arange(m_eff), k0 + np.arange(m_eff)] = 1.0
+        ys = nf4.nf4_gemm_grouped(_x_tensor(_to16(x, "bf16"), "bf16", M, K), members, K=K, y_dtype="f32",
+                                  workspace=ws)
+        torch.cuda.synchronize()
+        for i in range(len(Ns)):
+            w_gpu[i][:, k0:k0 + m_eff] = ys[i].cpu().numpy()[:m_eff].T
+    for i, N in enumerate(Ns):
+        want = orc.dequantize(packs[i], N * K, 64, orc.OUT_BF16, threads=8, **kws[i]).view(
+            ml_dtypes.bfloat16).astype(np.float32).reshape(N, K)
+        assert np.array_equal(_pos0(w_gpu[i]), _pos0(want)), (M, i)
