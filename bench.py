@@ -3,31 +3,42 @@
 
 A *step* is one pass of the whole hot path over a model's NF4 linear weights
 (all 7 projections of every decoder layer) -- what one inference forward
-pass dequantizes.  Default workload (N=1): BASELINE.json configs[1], the
-Gemma-3-27B linear-layer set, blocksize 64, double-quantized absmax, bf16
-output: 25.6 G elements, 64.4 GB of algorithmic traffic per step (inputs and
-outputs far larger than the 126 MB L2, so no flush is needed).
+pass dequantizes.  Default workload: BASELINE.json configs[2], the Qwen3-32B
+linear weights (the paper's profiled model, Table I), blocksize 64,
+double-quantized absmax, fp16 output (the paper's output type): 31.2 G
+elements, 78.5 GB of algorithmic traffic per step at N=1 -- the largest
+configuration that fits one GPU and the one the metric's "1/2/4/8 GPUs" is
+quoted on.  Inputs and outputs are far larger than the 126 MB L2, so no flush
+is needed between steps.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2]
-                    [--inputs gaussian|hash] [--scaling weak|strong] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3]
+                    [--inputs gaussian|hash] [--scaling strong|weak] [--impl ours|reference]
 
-Multi-GPU (torchrun, one process per GPU): the path has no exchange step, so
-no data-path collective.  --scaling weak (default): every rank dequantizes its
-own full linear-weight set (independent replicas, seeds offset by rank);
---scaling strong: the model is row-sharded across ranks (config 3/4 style).
-Time is measured with CUDA events on the launching stream, max over ranks.
+Multi-GPU: one process per GPU.  Under torchrun (the driver) RANK/WORLD_SIZE come
+from the environment and must match --gpus; without torchrun, `--gpus N` > 1
+re-launches itself through torch.distributed.run on N local ranks.  The path has
+no exchange step, so there is no data-path collective: with
+--scaling strong (default) every weight is row-sharded N ways and each rank
+quantizes and dequantizes its own shards (what an N-GPU tensor-parallel
+deployment holds); --scaling weak gives every rank a full model replica.  Time
+is measured with CUDA events on the launching stream, max over ranks; NCCL
+carries only the barrier and that max.
 
-Rank 0 prints ONE JSON line.  `value` is whole-job algorithmic GB/s
-(codes ceil(n/2) + scales + 2 B/elt output), `e2e` the same metric
-through the host-buffer C-ABI call (pinned host -> HBM -> host, copies timed),
-`roofline` the dequant kernel against the measured HBM copy peak,
-`cpu_baseline` the CPU oracle on a bounded sample on this host's cores.
+Rank 0 prints ONE JSON line: `value` = whole-job algorithmic GB/s (SURVEY 8(d):
+codes ceil(n/2) + scales + 2 B/elt output), `e2e` the same metric through the
+host-buffer C-ABI call (pinned host -> HBM -> host, copies timed), `roofline`
+the dequant kernel against the measured HBM copy peak (from the timed pass),
+`cpu_baseline` the CPU oracle on a bounded sample on this host's cores (all
+threads and one thread), `extra_configs` the same step on config 2 (Gemma-3-27B,
+bf16), and `f1` the fused NF4 dequant + tcgen05 GEMM over 8
+Gemma-3-27B decoder layers at M = 1 / 16 / 64 tokens.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -44,6 +55,7 @@ from synth import workloads as wl  # noqa: E402
 
 METRIC = "NF4 dequant HBM GB/s & % of B200 peak, Gelem/s at 1/2/4/8 GPUs"
 UNIT = "GB/s"
+NOMINAL_HBM_GBS = 8000.0
 
 
 def _peaks():
@@ -122,15 +134,16 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 def oracle_sample_inputs(cfg, n):
     """Counter-based inputs for the first n elements of a tensor of the workload."""
+    from synth import fast
     c = wl.CONFIGS[cfg]
     bs = c.blocksize
     nb = -(-n // bs)
-    packed = syn.hash_packed(7, 0, (n + 1) // 2)
+    packed = fast.packed(7, 0, (n + 1) // 2)
     if c.dq:
-        kw = dict(qabsmax=syn.hash_qabsmax(7, 0, nb), code2=syn.dynamic_map_code2(),
-                  absmax2=syn.hash_absmax2(7, 0, -(-nb // 256)), offset=float(syn.hash_offset(7)))
+        kw = dict(qabsmax=fast.qabsmax(7, 0, nb), code2=syn.dynamic_map_code2(),
+                  absmax2=fast.absmax2(7, 0, -(-nb // 256)), offset=float(syn.hash_offset(7)))
     else:
-        kw = dict(absmax=syn.hash_absmax(7, 0, nb))
+        kw = dict(absmax=fast.absmax(7, 0, nb))
     return packed, kw
 
 
@@ -151,7 +164,7 @@ def size_oracle_sample(cfg, target_s, threads):
     import oracle
     c = wl.CONFIGS[cfg]
     code = oracle.OUT_F16 if c.out_dtype == "f16" else oracle.OUT_BF16
-    probe_n = 1 << 25   # 64 MB of output: larger than the host caches, like the sample
+    probe_n = (1 << 25) if threads > 1 else (1 << 23)   # larger than the host caches, like the sample
     packed, kw = oracle_sample_inputs(cfg, probe_n)
     oracle.dequantize(packed, 1 << 20, c.blocksize, code, threads=threads, **kw)   # load + warm up
     t0 = time.perf_counter()
@@ -198,7 +211,17 @@ def time_oracle(cfg, target_s=10.0, threads=None, n=None):
                       + (f" dequantized {passes} times" if passes > 1 else "")
                       + f" with the workload blocksize, absmax mode and output dtype "
                       f"(counter-based inputs; {c.description}), "
-                      f"{threads} threads, scalar C oracle"}
+                      f"{threads} thread{'s' if threads > 1 else ''}, scalar C oracle"}
+
+
+def cpu_baseline(cfg, target_s):
+    """The oracle on all host threads (the reported baseline) and on one thread
+    (1-thread and T-thread numbers, the paper's protocol P:406)."""
+    multi = time_oracle(cfg, target_s=target_s)
+    one = time_oracle(cfg, target_s=max(1.0, target_s / 2), threads=1)
+    multi["one_thread"] = {k: one[k] for k in ("value", "gelem_per_s", "seconds", "sample")}
+    multi["threads_speedup"] = round(multi["gelem_per_s"] / max(one["gelem_per_s"], 1e-9), 2)
+    return multi
 
 
 def run_reference(args, rank, world):
@@ -232,15 +255,62 @@ def run_reference(args, rank, world):
 
 
 # ---------------------------------------------------------------------------
+# work assignment and the cross-rank reduction (the only cross-rank traffic)
+# ---------------------------------------------------------------------------
+def rank_tensors(cfg: str, scaling: str, world: int, rank: int, layers=None):
+    """Tensors rank `rank` dequantizes: its row shard of every weight (strong)
+    or a full linear-weight set of its own (weak)."""
+    if scaling == "strong":
+        return wl.config_tensors(cfg, world_size=world, rank=rank, layers=layers)
+    return wl.config_tensors(cfg, layers=layers)
+
+
+def rank_seed0(cfg: str, rank: int) -> int:
+    return 1000 * int(cfg[-1]) + 100000 * rank
+
+
+def alg_bytes_of(tensors, blocksize: int, dq: bool) -> int:
+    """SURVEY 8(d) algorithmic bytes of one pass over `tensors` (== WeightStore.algorithmic_bytes)."""
+    tot = 0
+    for t in tensors:
+        nb = -(-t.n // blocksize)
+        tot += (t.n + 1) // 2 + 2 * t.n + ((nb + 4 * (-(-nb // 256))) if dq else 4 * nb)
+    return tot + (1024 if dq and tensors else 0)
+
+
+def reduce_over_ranks(ms: float, alg_bytes: float, elems: float, device, world: int):
+    """Max of the per-rank timed-region milliseconds and sum of the per-rank work
+    (algorithmic bytes, elements) -- the only cross-rank traffic of the path."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    u = torch.tensor([alg_bytes, elems], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(u, op=dist.ReduceOp.SUM)
+    return float(t.item()), float(u[0].item()), float(u[1].item())
+
+
+def gather_per_rank(ms: float, device, world: int):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    if world == 1:
+        return [ms]
+    out = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(out, t)
+    return [float(x.item()) for x in out]
+
+
+# ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
-def build_store(args, rank, world, device):
-    from paper_2604_02556_b200 import weights
-    c = wl.CONFIGS[args.config]
-    tensors = rank_tensors(args.config, args.scaling, world, rank, args.layers)
-    seed0 = 1000 * int(args.config[-1]) + 100000 * rank
-    maker = weights.from_gaussian if args.inputs == "gaussian" else weights.from_hash
-    return maker(tensors, c.blocksize, c.dq, c.out_dtype, seed0=seed0, device=device), tensors
+def build_store(args, cfg, rank, world, device):
+    from synth import stores
+    c = wl.CONFIGS[cfg]
+    tensors = rank_tensors(cfg, args.scaling, world, rank, args.layers)
+    maker = stores.from_gaussian if args.inputs == "gaussian" else stores.from_hash
+    return maker(tensors, c.blocksize, c.dq, c.out_dtype, seed0=rank_seed0(cfg, rank), device=device), tensors
 
 
 def measure_sol(nf4, torch, in_bytes=2 << 30, reps=10):
@@ -263,9 +333,8 @@ def measure_sol(nf4, torch, in_bytes=2 << 30, reps=10):
 
 
 def run_e2e(nf4, torch, ws, args, max_host_bytes, device=None, world=1):
-    """Same metric through nf4_dequantize_host: pinned host inputs -> HBM ->
-    kernel -> pinned host outputs, copies inside the timed region."""
-    c = wl.CONFIGS[args.config]
+    """Same metric through nf4_dequantize_host_batched: pinned host inputs -> HBM
+    -> kernel -> pinned host outputs, copies inside the timed region."""
     bs = ws.blocksize
     # bounded prefix of the workload that fits the host-memory budget
     chosen, host_bytes = [], 0
@@ -324,51 +393,39 @@ def run_e2e(nf4, torch, ws, args, max_host_bytes, device=None, world=1):
     return {"value": round(alg_all / dt / 1e9, 2), "unit": UNIT, "h2d_bytes_per_step": int(h2d) * world,
             "d2h_bytes_per_step": int(d2h) * world, "ms_per_step": round(dt * 1e3, 2),
             "gelem_per_s": round(elems_all / dt / 1e9, 3),
-            "sample": f"first {len(chosen)} of {len(ws.entries)} tensors "
+            "sample": f"first {len(chosen)} of {len(ws.entries)} tensors per rank "
                       f"({sum(it[3] for it in items) / 1e9:.2f} G elements) through nf4_dequantize_host_batched, "
                       f"pinned host buffers, {chunk}-element chunks"}
 
 
-def reduce_over_ranks(ms: float, alg_bytes: float, elems: float, device, world: int):
-    """Max of the per-rank timed-region milliseconds and sum of the per-rank work
-    (algorithmic bytes, elements) -- the only cross-rank traffic of the path."""
-    import torch
+def ncu_traffic(cfg, inputs, variant, alg_per_launch):
+    """DRAM bytes per launch of the dequant kernel from the committed ncu capture
+    (profiles/ncu_traffic.json), scaled to this launch -- only if that capture was
+    taken on exactly these kernel sources (source hash), variant and workload;
+    otherwise None with the reason."""
+    from paper_2604_02556_b200 import _build
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            tr = json.load(f)
+    except Exception:
+        return None, "no ncu capture committed"
+    want = {"config": cfg, "inputs": inputs, "variant": variant, "source_hash": _build.source_hash()}
+    stale = [k for k, v in want.items() if tr.get(k) != v]
+    if stale:
+        return None, "ncu capture does not match this run (" + ", ".join(stale) + ")"
+    return int(tr["traffic_bytes_per_alg_byte"] * alg_per_launch), \
+        f"ncu --set full capture {tr.get('source', '')}: DRAM bytes / algorithmic = {tr['traffic_bytes_per_alg_byte']:.5f}"
+
+
+def measure_dequant(args, cfg, rank, world, device, nf4, torch, steps, full=True):
+    """Build the workload, warm up, time `steps` steps (max over ranks).  Returns
+    (result dict, store)."""
     import torch.distributed as dist
-    t = torch.tensor([ms], dtype=torch.float64, device=device)
-    u = torch.tensor([alg_bytes, elems], dtype=torch.float64, device=device)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(u, op=dist.ReduceOp.SUM)
-    return float(t.item()), float(u[0].item()), float(u[1].item())
-
-
-def rank_tensors(cfg: str, scaling: str, world: int, rank: int, layers=None):
-    """Tensors rank `rank` dequantizes: its row shard of every weight (strong)
-    or a full linear-weight set of its own (weak)."""
-    if scaling == "strong":
-        return wl.config_tensors(cfg, world_size=world, rank=rank, layers=layers)
-    return wl.config_tensors(cfg, layers=layers)
-
-
-def run_ours(args, rank, world, local_rank):
-    import torch
-    import torch.distributed as dist
-
-    import paper_2604_02556_b200 as nf4
     from paper_2604_02556_b200 import _lib
-
-    torch.cuda.set_device(local_rank)
-    device = torch.device("cuda", local_rank)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=device)
-    nf4.load()
-    if args.variant is not None:
-        nf4.nf4_set_kernel_variant(int(args.variant) if args.variant.isdigit() else args.variant)
-    variant = nf4.nf4_kernel_variants()[nf4.nf4_get_kernel_variant()]
-    c = wl.CONFIGS[args.config]
-
+    c = wl.CONFIGS[cfg]
     t_build = time.perf_counter()
-    ws, tensors = build_store(args, rank, world, device)
+    ws, tensors = build_store(args, cfg, rank, world, device)
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t_build
 
@@ -409,22 +466,24 @@ def run_ours(args, rank, world, local_rank):
         def flush():
             flush_sink.copy_(flush_buf.sum(dtype=torch.int64))
 
-    # kernel-level roofline pass: CUDA events around every launch, same stream
+    # diagnostic pass: CUDA events around every launch (breaks the PDL overlap
+    # between launches, so it is slightly slower than the timed pass below)
     kt = []
-    for _ in range(max(3, min(args.steps, 20))):
-        if cold:
-            flush()
-        step(launch_events)
-        torch.cuda.synchronize()
-        kt.append(sum(s.elapsed_time(e) for s, e in launch_events))
-    kernel_ms = statistics.median(kt)
+    if full:
+        for _ in range(max(3, min(steps, 20))):
+            if cold:
+                flush()
+            step(launch_events)
+            torch.cuda.synchronize()
+            kt.append(sum(s.elapsed_time(e) for s, e in launch_events))
 
-    sampler = ClockSampler(local_rank)
+    sampler = ClockSampler(device.index if device.index is not None else 0) if full else None
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    sampler.start()
-    time.sleep(0.3)
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
@@ -432,7 +491,7 @@ def run_ours(args, rank, world, local_rank):
     launches = 0
     if cold:
         step_events = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                       for _ in range(args.steps)]
+                       for _ in range(steps)]
         for s_ev, e_ev in step_events:
             flush()
             s_ev.record(stream)
@@ -440,33 +499,150 @@ def run_ours(args, rank, world, local_rank):
             e_ev.record(stream)
     else:
         start.record(stream)
-        for _ in range(args.steps):
+        for _ in range(steps):
             launches += step()
         end.record(stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    clocks = sampler.stop()
+    clocks = sampler.stop() if sampler else None
     ms = sum(s_ev.elapsed_time(e_ev) for s_ev, e_ev in step_events) if cold else start.elapsed_time(end)
+    per_rank_ms = gather_per_rank(ms, device, world)
     ms_max, tot_bytes, tot_elems = reduce_over_ranks(ms, float(ws.algorithmic_bytes()), float(ws.n_total),
                                                      device, world)
-    value = tot_bytes * args.steps / (ms_max * 1e-3) / 1e9
-    gelem = tot_elems * args.steps / (ms_max * 1e-3) / 1e9
+    value = tot_bytes * steps / (ms_max * 1e-3) / 1e9
+    gelem = tot_elems * steps / (ms_max * 1e-3) / 1e9
+    res = {"value": value, "gelem": gelem, "ms_max": ms_max, "ms_rank": ms, "per_rank_ms": per_rank_ms,
+           "launches": launches, "launches_per_step": len(carrs), "kt": kt, "clocks": clocks, "cold": cold,
+           "t_build": t_build, "tensors": tensors, "alg_per_step": ws.algorithmic_bytes(), "n_rank": ws.n_total,
+           "tot_bytes": tot_bytes, "tot_elems": tot_elems}
+    return res, ws
 
+
+def f1_layer_groups(tensors):
+    """Consecutive weights of one decoder layer that share X: (q,k,v), (o), (gate,up), (down)."""
+    groups, cur = [], []
+    for i, t in enumerate(tensors):
+        kind = t.name.split(".")[2].split("[")[0]
+        key = {"q_proj": "qkv", "k_proj": "qkv", "v_proj": "qkv", "gate_proj": "gu", "up_proj": "gu"}.get(kind, kind)
+        lay = t.name.split(".")[1]
+        if cur and (cur[0][1] != (lay, key) or key not in ("qkv", "gu")):
+            groups.append([c[0] for c in cur])
+            cur = []
+        cur.append((i, (lay, key)))
+    if cur:
+        groups.append([c[0] for c in cur])
+    return groups
+
+
+def measure_f1(nf4, torch, peak, ms_list=(1, 16, 64), layers=8, steps=20, warmup=5):
+    """Y_t = X_t . W_t^T for every linear weight of `layers`
+    Gemma-3-27B decoder layers (DQ NF4, bf16 X/Y), fused (nf4_gemm_grouped for
+    the weights sharing X, nf4_gemm otherwise) vs the unfused path the paper
+    optimizes (nf4_dequantize into a bf16 buffer, then cuBLAS via torch.matmul).
+    HBM roofline of the fused step: the bytes it must move (codes + qabsmax +
+    absmax2 + X + Y) over the measured copy peak."""
+    from synth import stores
+    tensors = wl.model_tensors("gemma-3-27b", layers=layers)
+    ws = stores.from_hash(tensors, 64, True, "bf16", seed0=77, device="cuda")
+    dqs = [nf4.DQ(ws._ptr(ws.scales, e.scale_off), ws.code2.data_ptr(), ws._ptr(ws.groups, e.group_off), e.offset)
+           for e in ws.entries]
+    groups = f1_layer_groups(tensors)
+    n_total = sum(t.n for t in tensors)
+    out = {"workload": f"Gemma-3-27B, {layers} decoder layers x 7 linear weights ({n_total / 1e9:.2f} G NF4 "
+                       f"weights, blocksize 64, double-quant), bf16 X and Y",
+           "launches_per_step": len(groups), "steps": steps}
+    wbuf = torch.empty(max(t.n for t in tensors), dtype=torch.bfloat16, device="cuda")
+    for M in ms_list:
+        xs = {}
+        for t in tensors:
+            if t.cols not in xs:
+                xs[t.cols] = torch.randn(M, t.cols, device="cuda").to(torch.bfloat16)
+        ys = [torch.empty(M, t.rows, dtype=torch.bfloat16, device="cuda") for t in tensors]
+        gws = {}
+        for g in groups:
+            Ns = tuple(tensors[i].rows for i in g)
+            K = tensors[g[0]].cols
+            b = (nf4.nf4_gemm_grouped_workspace_bytes(M, Ns, K) if len(g) > 1
+                 else nf4.nf4_gemm_workspace_bytes(M, Ns[0], K, 0))
+            gws[tuple(g)] = torch.zeros(max(16, b), dtype=torch.uint8, device="cuda")
+
+        def fused():
+            for g in groups:
+                K = tensors[g[0]].cols
+                if len(g) == 1:
+                    i = g[0]
+                    nf4.nf4_gemm(xs[K], ws._ptr(ws.codes, ws.entries[i].codes_off), None, dqs[i], N=tensors[i].rows,
+                                 K=K, y=ys[i], workspace=gws[tuple(g)])
+                else:
+                    members = [(ws._ptr(ws.codes, ws.entries[i].codes_off), None, dqs[i], tensors[i].rows) for i in g]
+                    nf4.nf4_gemm_grouped(xs[K], members, K=K, ys=[ys[i] for i in g], workspace=gws[tuple(g)])
+
+        def unfused():
+            for i, (t, e) in enumerate(zip(tensors, ws.entries)):
+                nf4.nf4_dequantize(ws._ptr(ws.codes, e.codes_off), None, dqs[i], n=e.n, blocksize=64,
+                                   out_dtype="bf16", out=wbuf)
+                torch.matmul(xs[t.cols], wbuf[:e.n].view(t.rows, t.cols).t(), out=ys[i])
+
+        def timeit(fn):
+            for _ in range(warmup):
+                fn()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(steps):
+                fn()
+            b.record()
+            torch.cuda.synchronize()
+            return a.elapsed_time(b) / steps
+
+        f_ms = timeit(fused)
+        u_ms = timeit(unfused)
+        wbytes = sum(e.n // 2 + e.n // 64 + 4 * (e.n // 64 // 256) for e in ws.entries) + 1024
+        xybytes = sum(2 * M * (t.cols + t.rows) for t in tensors)
+        gbs = (wbytes + xybytes) / (f_ms * 1e-3) / 1e9
+        out[f"M{M}"] = {"fused_ms": round(f_ms, 4), "unfused_ms": round(u_ms, 4),
+                        "speedup_vs_dequant_plus_cublas": round(u_ms / f_ms, 3),
+                        "weights_per_s_T": round(n_total / (f_ms * 1e-3) / 1e12, 3),
+                        "tflops": round(2.0 * M * n_total / (f_ms * 1e-3) / 1e12, 2),
+                        "hbm_gbs": round(gbs, 1), "hbm_frac": round(gbs / peak, 4),
+                        "bytes_per_step": wbytes + xybytes}
+        del xs, ys, gws
+    del ws, wbuf
+    torch.cuda.empty_cache()
+    return out
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2604_02556_b200 as nf4
+
+    if torch.cuda.device_count() < world:
+        raise SystemExit(f"bench.py: {world} ranks but only {torch.cuda.device_count()} visible GPUs")
+    torch.cuda.set_device(local_rank)
+    device = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    nf4.load()
+    if args.variant is not None:
+        nf4.nf4_set_kernel_variant(int(args.variant) if args.variant.isdigit() else args.variant)
+    variant = nf4.nf4_kernel_variants()[nf4.nf4_get_kernel_variant()]
+    c = wl.CONFIGS[args.config]
     peak, peak_src = _peaks()
-    alg_per_step = ws.algorithmic_bytes()
-    achieved = alg_per_step / (kernel_ms * 1e-3) / 1e9
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
-        try:
-            with open(tpath) as f:
-                tr = json.load(f)
-            if tr.get("config") == args.config and tr.get("inputs", args.inputs) == args.inputs:
-                traffic = tr.get("traffic_bytes_per_alg_byte")
-                traffic = None if traffic is None else int(traffic * alg_per_step / len(carrs))
-        except Exception:
-            traffic = None
+
+    r, ws = measure_dequant(args, args.config, rank, world, device, nf4, torch, args.steps)
+    alg_per_step = r["alg_per_step"]
+    ms_per_step = r["ms_max"] / args.steps
+    # roofline of the dominant (and only) kernel in the timed region: every launch there is
+    # nf4::dequant_kernel, so its average launch duration is the timed region over the launches,
+    # and the bytes of one launch are its share of the step's algorithmic bytes
+    kernel_ms_per_launch = r["ms_rank"] / max(1, r["launches"])
+    alg_per_launch = alg_per_step / r["launches_per_step"]
+    achieved = alg_per_launch / (kernel_ms_per_launch * 1e-3) / 1e9
+    traffic, traffic_note = ncu_traffic(args.config, args.inputs, variant, alg_per_launch)
+    kt = r["kt"]
 
     extra = {}
     if rank == 0 and not args.no_sol:
@@ -480,56 +656,125 @@ def run_ours(args, rank, world, local_rank):
             avail = 16 << 30
         budget = int(min(avail // (4 * max(world, 1)), args.e2e_host_gb * (1 << 30)))
         e2e = run_e2e(nf4, torch, ws, args, budget, device=device, world=world)
+    del ws
+    torch.cuda.empty_cache()
 
-    cpu_baseline = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu_baseline = time_oracle(args.config, target_s=args.cpu_seconds)
+    extra_cfgs = {}
+    if world == 1 and args.extra_configs:
+        for cfg in [x for x in args.extra_configs.split(",") if x and x != args.config]:
+            rx, wsx = measure_dequant(args, cfg, rank, world, device, nf4, torch, max(10, args.steps // 2),
+                                      full=False)
+            del wsx
+            torch.cuda.empty_cache()
+            cx = wl.CONFIGS[cfg]
+            extra_cfgs[cfg] = {"workload": cx.description, "value": round(rx["value"], 1), "unit": UNIT,
+                               "gelem_per_s": round(rx["gelem"], 2),
+                               "ms_per_step": round(rx["ms_max"] / max(10, args.steps // 2), 4),
+                               "roofline_frac": round(rx["value"] / peak, 4),
+                               "pct_of_nominal_8000": round(100 * rx["value"] / NOMINAL_HBM_GBS, 2),
+                               "bytes_per_step": rx["alg_per_step"], "launches_per_step": rx["launches_per_step"],
+                               "steps": max(10, args.steps // 2), "cold_l2": rx["cold"]}
+
+    f1 = None
+    if world == 1 and not args.no_f1:
+        f1 = measure_f1(nf4, torch, peak)
+
+    cb = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cb = cpu_baseline(args.config, target_s=args.cpu_seconds)
+    if world > 1:
+        dist.barrier()
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
+            "metric": METRIC, "value": round(r["value"], 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
             "scaling": args.scaling, "vs_baseline": None,
             "dtype": f"u8->{c.out_dtype}",
             "data": ("synthetic: W~N(0,0.02^2) per tensor (torch on device), quantized by nf4_quantize"
                      + (" + nf4_double_quantize" if c.dq else "")) if args.inputs == "gaussian"
                     else "synthetic: counter-based hash codes/scales (synth.inputs)",
             "config": {"workload": c.description, "key": args.config,
-                       "model": c.model or "single 4096x4096", "tensors_per_rank": len(tensors),
-                       "elements_per_rank": ws.n_total, "blocksize": c.blocksize,
-                       "absmax": "double-quant" if c.dq else "fp32", "out_dtype": c.out_dtype,
-                       "algorithmic_bytes_per_step_per_rank": alg_per_step,
-                       "launches_per_step": len(carrs), "kernel_variant": variant,
+                       "model": c.model or "single 4096x4096", "tensors_per_rank": len(r["tensors"]),
+                       "elements_per_rank": r["n_rank"], "elements_total": int(r["tot_elems"]),
+                       "blocksize": c.blocksize, "absmax": "double-quant" if c.dq else "fp32",
+                       "out_dtype": c.out_dtype, "algorithmic_bytes_per_step_per_rank": alg_per_step,
+                       "algorithmic_bytes_per_step_total": int(r["tot_bytes"]),
+                       "launches_per_step": r["launches_per_step"], "kernel_variant": variant,
                        "l2": "inputs+outputs per step >> 126 MB L2 (no flush needed)"
-                             if not cold else "L2 flushed (512 MB read) before every timed step; "
-                                              "time = sum of per-step CUDA-event intervals",
-                       "parallelism": f"{args.scaling}-dp{world}" if world > 1 else "single GPU"},
-            "gelem_per_s": round(gelem, 2),
-            "pct_of_peak": {"measured_copy_6551.7": round(100 * value / world / peak, 2),
-                            "nominal_8000": round(100 * value / world / 8000.0, 2)},
+                             if not r["cold"] else "L2 flushed (512 MB read) before every timed step; "
+                                                   "time = sum of per-step CUDA-event intervals",
+                       "parallelism": (f"row-sharded {world} ways (each rank its own shard of every weight), "
+                                       "no data-path collective" if args.scaling == "strong"
+                                       else f"{world} independent replicas") if world > 1 else "single GPU"},
+            "gelem_per_s": round(r["gelem"], 2),
+            "pct_of_peak": {"measured_copy_%.1f" % peak: round(100 * r["value"] / world / peak, 2),
+                            "nominal_8000": round(100 * r["value"] / world / NOMINAL_HBM_GBS, 2)},
+            "per_rank_ms_per_step": [round(x / args.steps, 4) for x in r["per_rank_ms"]],
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": UNIT,
-                         "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "nf4::dequant_kernel", "kernel_ms_per_step": round(kernel_ms, 4),
-                         "bytes_per_step": alg_per_step,
-                         # SURVEY 8(d) timing protocol over the per-step kernel times of this pass:
-                         # median (the headline `achieved`), min / max, and the paper's
+                         "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_note,
+                         "peak_source": peak_src, "kernel": "nf4::dequant_kernel",
+                         "timing": "timed region of this run (rank 0) / its launches; every launch there is "
+                                   "this kernel",
+                         "kernel_ms_per_launch": round(kernel_ms_per_launch, 4),
+                         "bytes_per_launch": int(alg_per_launch),
+                         "pct_of_nominal_8000": round(100 * achieved / NOMINAL_HBM_GBS, 2),
+                         # separate diagnostic pass with CUDA events around every launch (events between
+                         # launches break the PDL overlap): median / best / worst and the paper's
                          # "mean of 3 measured passes after 1 warm-up"
-                         "per_step_gbs": {"median": round(achieved, 1),
-                                          "best": round(alg_per_step / (min(kt) * 1e-3) / 1e9, 1),
-                                          "worst": round(alg_per_step / (max(kt) * 1e-3) / 1e9, 1),
-                                          "paper_mean_of_3": round(alg_per_step / (statistics.mean(kt[:3]) * 1e-3)
-                                                                   / 1e9, 1),
-                                          "passes": len(kt)}},
+                         "per_launch_events_gbs": None if not kt else {
+                             "median": round(alg_per_step / (statistics.median(kt) * 1e-3) / 1e9, 1),
+                             "best": round(alg_per_step / (min(kt) * 1e-3) / 1e9, 1),
+                             "worst": round(alg_per_step / (max(kt) * 1e-3) / 1e9, 1),
+                             "paper_mean_of_3": round(alg_per_step / (statistics.mean(kt[:3]) * 1e-3) / 1e9, 1),
+                             "passes": len(kt)}},
             "e2e": e2e,
-            "cpu_baseline": cpu_baseline,
-            "gpu_launches": launches,
-            "clocks": clocks,
-            "setup_seconds": round(t_build, 1),
+            "cpu_baseline": cb,
+            "gpu_launches": r["launches"],
+            "clocks": r["clocks"],
+            "setup_seconds": round(r["t_build"], 1),
         }
+        if extra_cfgs:
+            line["extra_configs"] = extra_cfgs
+        if f1 is not None:
+            line["f1"] = f1
         line.update(extra)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_dry(args, rank, world):
+    """--dry-run: the multi-rank harness without a GPU (gloo): work assignment,
+    algorithmic bytes, the cross-rank reduction and the single JSON line, with a
+    synthetic per-rank time.  Used by the CPU tests of the launch path."""
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("gloo")
+    c = wl.CONFIGS[args.config]
+    tensors = rank_tensors(args.config, args.scaling, world, rank, args.layers)
+    alg = alg_bytes_of(tensors, c.blocksize, c.dq)
+    ms = alg / 6.5e9 * args.steps * (1.0 + 0.01 * rank)
+    per_rank = gather_per_rank(ms, "cpu", world)
+    ms_max, tot_b, tot_e = reduce_over_ranks(ms, float(alg), float(sum(t.n for t in tensors)), "cpu", world)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": round(tot_b * args.steps / (ms_max * 1e-3) / 1e9, 1),
+                          "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                          "scaling": args.scaling, "dry_run": True,
+                          "config": {"key": args.config, "elements_total": int(tot_e),
+                                     "algorithmic_bytes_per_step_total": int(tot_b),
+                                     "tensors_per_rank": len(tensors)},
+                          "per_rank_ms_per_step": [x / args.steps for x in per_rank]}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
 
 
 def main():
@@ -537,15 +782,18 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="cfg2", choices=sorted(wl.CONFIGS))
+    ap.add_argument("--config", default="cfg3", choices=sorted(wl.CONFIGS))
     ap.add_argument("--layers", type=int, default=None, help="limit to the first L decoder layers")
     ap.add_argument("--inputs", default="gaussian", choices=["gaussian", "hash"])
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--variant", default=None, help="dequant kernel variant (name or index)")
+    ap.add_argument("--extra-configs", default="cfg2", help="comma list measured after the main config (N=1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sol", action="store_true")
+    ap.add_argument("--no-f1", action="store_true")
+    ap.add_argument("--dry-run", action="store_true", help="no GPU: exercise the multi-rank harness with gloo")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-step-seconds", type=float, default=None,
                     help="oracle seconds per reference step (default: ~90 s / (steps + warmup), 0.2..5 s)")
@@ -555,11 +803,23 @@ def main():
     if args.warmup < 3 and args.impl == "ours":
         print("note: warmup raised to 3 (timing rule)", file=sys.stderr)
         args.warmup = 3
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None and args.gpus > 1:
+        # not under torchrun: launch N local ranks of this same command
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] \
+            + sys.argv[1:]
+        sys.exit(subprocess.call(cmd, cwd=ROOT))
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world = int(env_world or "1")
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.dry_run:
+        run_dry(args, rank, world)
         return
     run_ours(args, rank, world, local_rank)
 

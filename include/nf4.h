@@ -139,7 +139,10 @@ int64_t nf4_host_workspace_bytes(int64_t chunk_elems, int32_t blocksize, int32_t
  * in the descriptors (packed, absmax, dq.*, out) is a [host] pointer.  The
  * workspace must hold nf4_host_workspace_bytes(chunk_elems, smallest blocksize,
  * any tensor double-quantized); chunk_elems must be a multiple of 256 x the
- * largest blocksize.  Synchronous like nf4_dequantize_host.
+ * largest blocksize.  fp32-absmax and double-quant tensors may be mixed: every
+ * workspace slot reserves 4 B of scales per block of the smallest blocksize
+ * (the widest scale slice a chunk can need), so no copy spills into a slot's
+ * output region.  Synchronous like nf4_dequantize_host.
  */
 nf4_status nf4_dequantize_host_batched(const nf4_tensor* tensors, int32_t count, nf4_dtype out_dtype,
                                        void* workspace, int64_t workspace_bytes, int64_t chunk_elems,

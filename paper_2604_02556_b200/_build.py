@@ -65,6 +65,19 @@ def build_variant(name: str, defines: dict) -> str:
     return out
 
 
+def source_hash() -> str:
+    """Hash of every source the library is built from (kernels, headers, build
+    flags): keys measurements such as profiles/ncu_traffic.json to the exact
+    kernel code they were taken on."""
+    import hashlib
+    h = hashlib.sha256()
+    h.update(" ".join(NVCC_FLAGS).encode())
+    for s in SOURCES + HEADERS:
+        with open(os.path.join(CSRC, s), "rb") as f:
+            h.update(s.encode() + b"\0" + f.read())
+    return h.hexdigest()[:16]
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)
     print(LIB)

@@ -35,6 +35,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <type_traits>
 
@@ -1005,10 +1006,17 @@ static cudaError_t launch1(const GemmParams& p, const CodeMaps& mc, const CUtens
   static_assert(sm + 6 * 1024 <= 232448, "shared-memory budget (stages + pair table) exceeded");
   static_assert(nacc_for<BN>() * (BN < 32 ? 32 : BN) + groups_for<BN>() * sub_for<BN>() * 32 <= 512, "TMEM budget");
   static_assert(cst_for<BN>() >= groups_for<BN>(), "a super-stage slot must not be two phases behind any group");
-  static std::once_flag once;          // per instantiation (per process: one device type)
-  static cudaError_t attr = cudaSuccess;
-  std::call_once(once, [&] { attr = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)); });
-  if (attr != cudaSuccess) return attr;
+  // the dynamic shared-memory opt-in is a per-device (per-context) attribute: set it once
+  // per device and instantiation, and never cache a failure
+  static std::atomic<uint64_t> attr_set{0};  // bit d: set on device d (d < 64; others set every call)
+  int dev = 0;
+  if (const cudaError_t e = cudaGetDevice(&dev); e != cudaSuccess) return e;
+  const uint64_t bit = dev >= 0 && dev < 64 ? uint64_t(1) << dev : 0;
+  if (!bit || !(attr_set.load(std::memory_order_acquire) & bit)) {
+    const cudaError_t a = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+    if (a != cudaSuccess) return a;
+    attr_set.fetch_or(bit, std::memory_order_acq_rel);
+  }
   // launched with programmatic stream serialization (the kernel executes
   // griddepcontrol.wait before reading any input)
   cudaLaunchConfig_t cfg = {};

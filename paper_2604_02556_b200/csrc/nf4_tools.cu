@@ -143,7 +143,10 @@ HostLayout host_layout(int64_t chunk, int32_t bs, bool dq) {
   HostLayout L;
   const int64_t nb = chunk / bs;
   L.codes = rnd(chunk / 2);
-  L.scales = rnd(dq ? nb : nb * 4);
+  // fp32 absmax width even when dq: a batch may mix fp32-absmax and double-quant
+  // tensors, and the slot must hold the widest scale slice of a chunk (4 B per block)
+  (void)dq;
+  L.scales = rnd(nb * 4);
   L.groups = dq ? rnd((nb / 256) * 4) : 0;
   L.code2 = dq ? 1024 : 0;
   L.out = rnd(chunk * 2);

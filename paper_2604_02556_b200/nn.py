@@ -15,6 +15,7 @@ from __future__ import annotations
 
 from typing import Optional
 
+import numpy as np
 import torch
 
 from . import DQ, nf4_dequantize, nf4_double_quantize, nf4_gemm, nf4_gemm_workspace_bytes, nf4_quantize
@@ -22,7 +23,8 @@ from . import DQ, nf4_dequantize, nf4_double_quantize, nf4_gemm, nf4_gemm_worksp
 
 class NF4Linear(torch.nn.Module):
     def __init__(self, in_features: int, out_features: int, blocksize: int = 64, double_quant: bool = True,
-                 compute_dtype: torch.dtype = torch.bfloat16, device=None, fused_max_m: int = 128):
+                 compute_dtype: torch.dtype = torch.bfloat16, device=None, fused_max_m: int = 128,
+                 bias: bool = False):
         super().__init__()
         if compute_dtype not in (torch.bfloat16, torch.float16):
             raise ValueError("compute_dtype must be bfloat16 or float16")
@@ -38,11 +40,14 @@ class NF4Linear(torch.nn.Module):
             self.register_buffer("qabsmax", torch.zeros(nb, dtype=torch.uint8, device=dev))
             self.register_buffer("absmax2", torch.zeros(-(-nb // 256), dtype=torch.float32, device=dev))
             self.register_buffer("code2", torch.zeros(256, dtype=torch.float32, device=dev))
+            # the DQ offset is state (saved / loaded with the weights); `offset` is its
+            # host copy, so forward never syncs to read it
+            self.register_buffer("dq_offset", torch.zeros((), dtype=torch.float32, device=dev))
             self.offset = 0.0
             self.absmax = None
         else:
             self.register_buffer("absmax", torch.zeros(nb, dtype=torch.float32, device=dev))
-        self.bias: Optional[torch.Tensor] = None
+        self.register_buffer("bias", torch.zeros(out_features, dtype=compute_dtype, device=dev) if bias else None)
         self._wbuf: Optional[torch.Tensor] = None
         self._gemm_ws: dict = {}     # M -> zero-initialised stream-K workspace (kept zeroed by nf4_gemm)
 
@@ -54,7 +59,7 @@ class NF4Linear(torch.nn.Module):
         """Quantize a dense [out, in] weight on the GPU (nf4_quantize, + nf4_double_quantize
         with offset = mean(absmax) and the BNB signed dynamic code table by default)."""
         out_f, in_f = weight.shape
-        m = cls(in_f, out_f, blocksize, double_quant, compute_dtype, weight.device, fused_max_m)
+        m = cls(in_f, out_f, blocksize, double_quant, compute_dtype, weight.device, fused_max_m, bias is not None)
         w = weight.detach().contiguous()
         if w.dtype not in (torch.float32, torch.float16, torch.bfloat16):
             w = w.float()
@@ -62,16 +67,22 @@ class NF4Linear(torch.nn.Module):
             absmax = torch.empty(m.qabsmax.numel(), dtype=torch.float32, device=w.device)
             nf4_quantize(w.reshape(-1), blocksize, packed=m.packed, absmax=absmax)
             if code2 is None:
-                from synth import inputs as syn  # the BNB table is plain data (an input)
-                code2 = torch.from_numpy(syn.dynamic_map_code2())
+                from .tables import bnb_dynamic_code2  # the BNB table is plain data (an input)
+                code2 = torch.from_numpy(bnb_dynamic_code2())
             m.code2.copy_(code2.to(device=w.device, dtype=torch.float32))
-            m.offset = float(absmax.double().mean().item())
+            m.offset = float(np.float32(absmax.double().mean().item()))
+            m.dq_offset.fill_(m.offset)
             nf4_double_quantize(absmax, m.offset, m.code2, qabsmax=m.qabsmax, absmax2=m.absmax2)
         else:
             nf4_quantize(w.reshape(-1), blocksize, packed=m.packed, absmax=m.absmax)
         if bias is not None:
-            m.bias = bias.detach().to(compute_dtype).clone()
+            m.bias.copy_(bias.detach().to(compute_dtype))
         return m
+
+    def _load_from_state_dict(self, state_dict, prefix, *args, **kwargs):
+        super()._load_from_state_dict(state_dict, prefix, *args, **kwargs)
+        if self.double_quant:
+            self.offset = float(self.dq_offset)
 
     def _dq(self) -> Optional[DQ]:
         return DQ(self.qabsmax, self.code2, self.absmax2, self.offset) if self.double_quant else None

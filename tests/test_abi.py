@@ -151,3 +151,22 @@ def test_product_never_imports_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
                 assert "oracle.h" not in src and "liboracle" not in src, f
+
+
+def test_product_never_imports_test_inputs():
+    """The product package does not import synth/ (the test-input generators)."""
+    pkg = os.path.join(ROOT, "paper_2604_02556_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith(".py"):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "import synth" not in src and "from synth" not in src, f
+
+
+def test_package_code2_table_equals_test_input_table():
+    import numpy as np
+    from paper_2604_02556_b200.tables import bnb_dynamic_code2
+    from synth import inputs as syn
+    a, b = bnb_dynamic_code2(), syn.dynamic_map_code2()
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    assert a[127] == 0.0 and a[255] == 1.0 and np.all(np.diff(a) > 0)

@@ -18,7 +18,8 @@ def test_bench_json_line_contract():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "cfg1", "--steps", "5",
-                          "--warmup", "3", "--cpu-seconds", "1"], capture_output=True, text=True, timeout=600,
+                          "--warmup", "3", "--cpu-seconds", "1",
+                          "--extra-configs", ""], capture_output=True, text=True, timeout=600,
                          cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [l for l in out.stdout.splitlines() if l.strip().startswith("{")]
@@ -38,3 +39,8 @@ def test_bench_json_line_contract():
     c = d["cpu_baseline"]
     assert c["kind"] == "oracle" and c["cores"] >= 1 and c["value"] > 0
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+    assert c["one_thread"]["value"] > 0 and c["one_thread"]["gelem_per_s"] <= c["gelem_per_s"] * 1.5
+    f = d["f1"]
+    for m in ("M1", "M16", "M64"):
+        assert f[m]["fused_ms"] > 0 and f[m]["speedup_vs_dequant_plus_cublas"] > 0 and 0 < f[m]["hbm_frac"] < 1.2
+    assert d["roofline"]["kernel_ms_per_launch"] > 0

@@ -109,10 +109,10 @@ def _check_store_full(ws, orc, pinned):
 
 def _run_store(nf4, orc, pinned, key, tensors, seed0, label):
     import torch
-    from paper_2604_02556_b200 import weights
+    from synth import stores
     c = wl.CONFIGS[key]
     t0 = time.perf_counter()
-    ws = weights.from_hash(tensors, c.blocksize, c.dq, c.out_dtype, seed0=seed0, device="cuda")
+    ws = stores.from_hash(tensors, c.blocksize, c.dq, c.out_dtype, seed0=seed0, device="cuda")
     ws.out.fill_(0x7F)                       # no stale output can pass
     launches = ws.dequantize_all()
     torch.cuda.synchronize()

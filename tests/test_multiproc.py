@@ -85,3 +85,40 @@ def test_torchrun_reference_arm_rank0_only():
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["cpu_baseline"]["kind"] == "oracle" and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["n_gpus"] == 2
+
+
+def test_bench_self_launches_n_ranks_dry_run():
+    """`python bench.py --gpus 2` without torchrun re-launches itself on 2 local
+    ranks (torch.distributed.run); --dry-run replaces the GPU work with a
+    synthetic time (gloo), so the whole launch path runs here: exactly one JSON
+    line, n_gpus 2, strong scaling whose row shards cover Qwen3-32B exactly once."""
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run", "--steps", "2",
+                        "--warmup", "3"], capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["config"]["key"] == "cfg3"
+    assert d["config"]["elements_total"] == 31_205_621_760
+    assert len(d["per_rank_ms_per_step"]) == 2
+    # value = summed work over the slowest rank's time
+    assert d["value"] == round(d["config"]["algorithmic_bytes_per_step_total"]
+                               / (max(d["per_rank_ms_per_step"]) * 1e-3) / 1e9, 1)
+
+
+def test_bench_world_size_mismatch_is_an_error():
+    env = dict(os.environ, RANK="0", WORLD_SIZE="1", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run"],
+                       capture_output=True, text=True, timeout=120, cwd=ROOT, env=env)
+    assert r.returncode != 0 and "WORLD_SIZE" in r.stderr
+
+
+def test_alg_bytes_match_store_formula():
+    sys.path.insert(0, ROOT)
+    import bench
+    from synth import workloads as wl
+    t = wl.config_tensors("cfg3")
+    assert bench.alg_bytes_of(t, 64, True) == 78_509_261_824      # SURVEY 8(d): 78.51 GB per Qwen3 step
+    t = wl.config_tensors("cfg1")
+    assert bench.alg_bytes_of(t, 64, False) == 42_991_616

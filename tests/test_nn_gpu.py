@@ -75,3 +75,27 @@ def test_nf4lineargroup_matches_members(nn):
             ref, mag = xd @ wd.T, xd.abs() @ wd.abs().T
             bound = in_f * 2.0 ** -23 * mag * (1 + 2.0 ** -8) + ref.abs() * 2.0 ** -8 + 1e-30
             assert ((y.double() - ref).abs() <= bound).all(), M
+
+
+def test_nf4linear_state_dict_round_trip_keeps_offset_and_bias():
+    """the double-quant offset and the bias are module state; a
+    save/load round trip into a fresh layer gives identical outputs."""
+    import io
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2604_02556_b200.nn import NF4Linear
+    torch.manual_seed(0)
+    w = torch.randn(384, 512, device="cuda") * 0.02
+    b = torch.randn(384, device="cuda")
+    a = NF4Linear.from_weight(w, bias=b)
+    assert a.offset != 0.0
+    buf = io.BytesIO()
+    torch.save(a.state_dict(), buf)
+    buf.seek(0)
+    fresh = NF4Linear(512, 384, bias=True, device="cuda")
+    fresh.load_state_dict(torch.load(buf))
+    assert fresh.offset == a.offset
+    x = torch.randn(8, 512, device="cuda", dtype=torch.bfloat16)
+    assert torch.equal(a(x), fresh(x))
+    assert torch.equal(a.dequantize(), fresh.dequantize())

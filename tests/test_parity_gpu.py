@@ -335,10 +335,10 @@ def _check_store_sampled(ws, orc, blocks_per_tensor=24, seed=0):
 @pytest.mark.parametrize("cfg", ["cfg1", "cfg2", "cfg3"])
 def test_full_size_configs_sampled(nf4, orc, cfg):
     import torch
-    from paper_2604_02556_b200 import weights
+    from synth import stores
     c = wl.CONFIGS[cfg]
     tensors = wl.config_tensors(cfg)
-    ws = weights.from_hash(tensors, c.blocksize, c.dq, c.out_dtype, seed0=1000 * int(cfg[-1]), device="cuda")
+    ws = stores.from_hash(tensors, c.blocksize, c.dq, c.out_dtype, seed0=1000 * int(cfg[-1]), device="cuda")
     ws.dequantize_all()
     n_checked = _check_store_sampled(ws, orc, blocks_per_tensor=8 if cfg != "cfg1" else 4096)
     assert n_checked > len(tensors)
@@ -355,9 +355,9 @@ def test_full_size_configs_sampled(nf4, orc, cfg):
 def test_llama_rank_shard_sampled(nf4, orc):
     """Config 4: rank 3 of the 8-way row sharding (each rank dequantizes its own shard)."""
     import torch
-    from paper_2604_02556_b200 import weights
+    from synth import stores
     tensors = wl.config_tensors("cfg4", world_size=8, rank=3)
-    ws = weights.from_hash(tensors, 64, True, "bf16", seed0=4000 + 3 * 100000, device="cuda")
+    ws = stores.from_hash(tensors, 64, True, "bf16", seed0=4000 + 3 * 100000, device="cuda")
     ws.dequantize_all()
     assert _check_store_sampled(ws, orc, blocks_per_tensor=4) > 0
     del ws
@@ -516,3 +516,32 @@ def test_host_buffer_batched_pipeline(nf4, orc):
     nf4.nf4_dequantize_host_batched(descs, "f16", workspace=ws, chunk_elems=chunk)
     for d, ref in zip(descs, refs):
         assert np.array_equal(d.out.numpy().view(np.uint16), ref)
+
+
+def test_host_buffer_batched_mixed_fp32_and_dq_small_blocks(nf4, orc):
+    """an fp32-absmax tensor at blocksize 64 in a batch that also
+    holds double-quant tensors (workspace sized for dq) must not spill its
+    scale copy into the slot's output region; several chunks per tensor so the
+    three slots are reused."""
+    import torch
+    chunk = 256 * 64 * 4
+    specs = [(5 * chunk + 4097, 64, False), (4 * chunk, 64, True), (3 * chunk + 64, 64, False), (2 * chunk, 128, True)]
+    ws = torch.empty(nf4.nf4_host_workspace_bytes(chunk, 64, True), dtype=torch.uint8, device="cuda")
+    descs, refs = [], []
+    for i, (n, bs, dq) in enumerate(specs):
+        packed, kw = _inputs(n, bs, dq, 1900 + i)
+        refs.append(_oracle(orc, packed, kw, n, bs, "bf16"))
+        out = torch.zeros(n, dtype=torch.int16).pin_memory()
+        pk = torch.from_numpy(packed).pin_memory()
+        if dq:
+            d = nf4.DQ(torch.from_numpy(kw["qabsmax"]).pin_memory(), torch.from_numpy(kw["code2"]).pin_memory(),
+                       torch.from_numpy(kw["absmax2"]).pin_memory(), kw["offset"])
+            descs.append(nf4.NF4Tensor(pk, n, bs, out, None, d))
+        else:
+            descs.append(nf4.NF4Tensor(pk, n, bs, out, torch.from_numpy(kw["absmax"]).pin_memory(), None))
+    for _ in range(2):
+        for d in descs:
+            d.out.zero_()
+        nf4.nf4_dequantize_host_batched(descs, "bf16", workspace=ws, chunk_elems=chunk)
+        for d, ref in zip(descs, refs):
+            assert np.array_equal(d.out.numpy().view(np.uint16), ref)

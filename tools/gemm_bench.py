@@ -27,7 +27,7 @@ def main():
     import torch
 
     import paper_2604_02556_b200 as nf4
-    from paper_2604_02556_b200 import weights
+    from synth import stores
     from synth import workloads as wl
 
     ap = argparse.ArgumentParser()
@@ -47,7 +47,7 @@ def main():
     torch.cuda.set_device(0)
     nf4.load()
     tensors = wl.model_tensors(args.model, layers=args.layers)
-    ws = weights.from_hash(tensors, 64, True, "bf16", seed0=7, device="cuda")
+    ws = stores.from_hash(tensors, 64, True, "bf16", seed0=7, device="cuda")
     M = args.m
     xs = {}
     for t in tensors:

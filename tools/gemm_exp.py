@@ -20,13 +20,13 @@ if not os.environ.get("NF4_LIB") and _exps_arg != "0":
 import torch
 
 import paper_2604_02556_b200 as nf4
-from paper_2604_02556_b200 import weights
+from synth import stores
 from synth import workloads as wl
 
 M, N, K = (int(v) for v in sys.argv[1:4]) if len(sys.argv) > 3 else (16, 21504, 5376)
 exps = [int(v) for v in sys.argv[4].split(",")] if len(sys.argv) > 4 else [0, 1, 2, 4, 6, 7]
 torch.cuda.set_device(0)
-ws = weights.from_hash([wl.Tensor("w", N, K)], 64, True, "bf16", 3, "cuda")
+ws = stores.from_hash([wl.Tensor("w", N, K)], 64, True, "bf16", 3, "cuda")
 e = ws.entries[0]
 dq = nf4.DQ(ws._ptr(ws.scales, e.scale_off), ws.code2.data_ptr(), ws._ptr(ws.groups, e.group_off), e.offset)
 x = torch.randn(M, K, device="cuda").to(torch.bfloat16)

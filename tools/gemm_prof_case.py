@@ -2,10 +2,10 @@ import sys, os
 sys.path.insert(0, os.getcwd())
 import torch
 import paper_2604_02556_b200 as nf4
-from paper_2604_02556_b200 import weights
+from synth import stores
 from synth import workloads as wl
 M, N, K, S = 16, 21504, 5376, int(sys.argv[1]) if len(sys.argv) > 1 else 0
-ws = weights.from_hash([wl.Tensor("w", N, K)], 64, True, "bf16", 3, "cuda")
+ws = stores.from_hash([wl.Tensor("w", N, K)], 64, True, "bf16", 3, "cuda")
 e = ws.entries[0]
 dq = nf4.DQ(ws._ptr(ws.scales, e.scale_off), ws.code2.data_ptr(), ws._ptr(ws.groups, e.group_off), e.offset)
 x = torch.randn(M, K, device="cuda").to(torch.bfloat16)

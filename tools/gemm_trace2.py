@@ -13,13 +13,13 @@ if not os.environ.get("NF4_LIB"):   # event traces / experiments need the diagno
 import torch
 
 import paper_2604_02556_b200 as nf4
-from paper_2604_02556_b200 import weights
+from synth import stores
 from synth import workloads as wl
 
 M, N, K = (int(v) for v in sys.argv[1:4]) if len(sys.argv) > 3 else (16, 21504, 5376)
 if len(sys.argv) > 4:
     os.environ["NF4_GEMM_EXPERIMENT"] = sys.argv[4]
-ws = weights.from_hash([wl.Tensor("w", N, K)], 64, True, "bf16", 3, "cuda")
+ws = stores.from_hash([wl.Tensor("w", N, K)], 64, True, "bf16", 3, "cuda")
 e = ws.entries[0]
 dq = nf4.DQ(ws._ptr(ws.scales, e.scale_off), ws.code2.data_ptr(), ws._ptr(ws.groups, e.group_off), e.offset)
 x = torch.randn(M, K, device="cuda").to(torch.bfloat16)

@@ -22,7 +22,7 @@ def main():
     import torch
 
     import paper_2604_02556_b200 as nf4
-    from paper_2604_02556_b200 import weights
+    from synth import stores
     from synth import workloads as wl
 
     ap = argparse.ArgumentParser()
@@ -31,7 +31,7 @@ def main():
     args = ap.parse_args()
     torch.cuda.set_device(0)
     tensors = wl.model_tensors(args.model, layers=1)
-    ws = weights.from_hash(tensors, 64, True, "bf16", seed0=11, device="cuda")
+    ws = stores.from_hash(tensors, 64, True, "bf16", seed0=11, device="cuda")
     descs = ws.nf4_tensors()
     s = torch.cuda.Stream()
     flush = torch.ones(512 << 20, dtype=torch.uint8, device="cuda")

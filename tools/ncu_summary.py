@@ -3,7 +3,7 @@
 
     python tools/ncu_summary.py --launches gpurun_out/launches_r01.csv \
         --rep gpurun_out/prof_dequant_r01.ncu-rep --alg-bytes-per-elem 2.515869 \
-        --out profiles/r01_ncu_summary.md --traffic-json profiles/ncu_traffic.json --config cfg2
+        --out profiles/r02_ncu_summary.md --traffic-json profiles/ncu_traffic.json --config cfg3
 
 * launch list (`--metrics gpu__time_duration.sum,dram__bytes_*`): per-kernel
   time share and per-launch DRAM bytes vs the algorithmic bytes of the launch
@@ -47,7 +47,8 @@ def main():
     ap.add_argument("--alg-bytes-per-elem", type=float, default=2.515869140625)
     ap.add_argument("--out", required=True)
     ap.add_argument("--traffic-json")
-    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--config", default="cfg3")
+    ap.add_argument("--variant", default="v2u4sxc", help="dequant kernel variant the capture ran")
     ap.add_argument("--title", default="ncu summary")
     a = ap.parse_args()
     lines = [f"# {a.title}", ""]
@@ -116,7 +117,14 @@ def main():
         f.write("\n".join(lines) + "\n")
     if a.traffic_json and ratios:
         with open(a.traffic_json, "w") as f:
-            json.dump({"config": a.config, "inputs": "gaussian",
+            import os
+            import sys
+            sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+            from paper_2604_02556_b200 import _build
+            # keyed to the kernel sources, variant and workload it was taken on: bench.py
+            # reports roofline.traffic only while all of these still match
+            json.dump({"config": a.config, "inputs": "gaussian", "variant": a.variant,
+                       "source_hash": _build.source_hash(),
                        "traffic_bytes_per_alg_byte": sum(ratios) / len(ratios),
                        "source": [a.launches, a.rep], "n_launches": len(ratios)}, f, indent=1)
     print("\n".join(lines))
