@@ -410,7 +410,7 @@ def ncu_traffic(cfg, inputs, variant, alg_per_launch):
             tr = json.load(f)
     except Exception:
         return None, "no ncu capture committed"
-    want = {"config": cfg, "inputs": inputs, "variant": variant, "source_hash": _build.source_hash()}
+    want = {"config": cfg, "inputs": inputs, "variant": variant, "source_hash": _build.source_hash(_build.DEQUANT_SOURCES)}
     stale = [k for k, v in want.items() if tr.get(k) != v]
     if stale:
         return None, "ncu capture does not match this run (" + ", ".join(stale) + ")"

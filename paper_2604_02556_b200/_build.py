@@ -65,18 +65,21 @@ def build_variant(name: str, defines: dict) -> str:
     return out
 
 
-def source_hash() -> str:
-    """Hash of every source the library is built from (kernels, headers, build
-    flags): keys measurements such as profiles/ncu_traffic.json to the exact
-    kernel code they were taken on."""
+DEQUANT_SOURCES = ["nf4_common.cu", "nf4_dequant.cu", "nf4_internal.cuh", os.path.join("..", "..", "include", "nf4.h")]
+
+
+def source_hash(files=None) -> str:
+    """Hash of the sources a kernel is built from (default: everything in the
+    library) plus the build flags: keys measurements such as
+    profiles/ncu_traffic.json (the dequant kernel: DEQUANT_SOURCES) to the exact
+    code they were taken on."""
     import hashlib
     h = hashlib.sha256()
     h.update(" ".join(NVCC_FLAGS).encode())
-    for s in SOURCES + HEADERS:
+    for s in (files if files is not None else SOURCES + HEADERS):
         with open(os.path.join(CSRC, s), "rb") as f:
             h.update(s.encode() + b"\0" + f.read())
     return h.hexdigest()[:16]
-
 
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)

@@ -124,7 +124,7 @@ def main():
             # keyed to the kernel sources, variant and workload it was taken on: bench.py
             # reports roofline.traffic only while all of these still match
             json.dump({"config": a.config, "inputs": "gaussian", "variant": a.variant,
-                       "source_hash": _build.source_hash(),
+                       "source_hash": _build.source_hash(_build.DEQUANT_SOURCES),
                        "traffic_bytes_per_alg_byte": sum(ratios) / len(ratios),
                        "source": [a.launches, a.rep], "n_launches": len(ratios)}, f, indent=1)
     print("\n".join(lines))
