@@ -30,8 +30,10 @@ host-buffer C-ABI call (pinned host -> HBM -> host, copies timed), `roofline`
 the dequant kernel against the measured HBM copy peak (from the timed pass),
 `cpu_baseline` the CPU oracle on a bounded sample on this host's cores (all
 threads and one thread), `extra_configs` the same step on config 2 (Gemma-3-27B,
-bf16), and `f1` the fused NF4 dequant + tcgen05 GEMM over 8
-Gemma-3-27B decoder layers at M = 1 / 16 / 64 tokens.
+bf16) and config 1 (one 4096x4096 tensor: L2-resident, so timed over rotating
+cold copies launched from one CUDA graph), and `f1` the fused NF4 dequant +
+tcgen05 GEMM over 8 Gemma-3-27B decoder layers at M = 1 / 16 /
+64 tokens.
 """
 from __future__ import annotations
 
@@ -305,12 +307,25 @@ def gather_per_rank(ms: float, device, world: int):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+L2_BYTES = 126e6
+
+
+def replicas_for(alg_bytes: int) -> int:
+    """Rotating copies of an L2-resident workload so that every timed step reads
+    and writes data last touched > 4 x L2 bytes earlier (cold), 1 otherwise."""
+    if alg_bytes > 8 * L2_BYTES:
+        return 1
+    return max(2, -(-int(4 * L2_BYTES) // max(1, alg_bytes)))
+
+
 def build_store(args, cfg, rank, world, device):
     from synth import stores
     c = wl.CONFIGS[cfg]
     tensors = rank_tensors(cfg, args.scaling, world, rank, args.layers)
+    reps = replicas_for(alg_bytes_of(tensors, c.blocksize, c.dq))
     maker = stores.from_gaussian if args.inputs == "gaussian" else stores.from_hash
-    return maker(tensors, c.blocksize, c.dq, c.out_dtype, seed0=rank_seed0(cfg, rank), device=device), tensors
+    return maker(tensors * reps, c.blocksize, c.dq, c.out_dtype, seed0=rank_seed0(cfg, rank), device=device), \
+        tensors, reps
 
 
 def measure_sol(nf4, torch, in_bytes=2 << 30, reps=10):
@@ -425,25 +440,32 @@ def measure_dequant(args, cfg, rank, world, device, nf4, torch, steps, full=True
     from paper_2604_02556_b200 import _lib
     c = wl.CONFIGS[cfg]
     t_build = time.perf_counter()
-    ws, tensors = build_store(args, cfg, rank, world, device)
+    ws, tensors, reps = build_store(args, cfg, rank, world, device)
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t_build
+    nt = len(tensors)
+    alg_step = alg_bytes_of(tensors, c.blocksize, c.dq)        # one pass over the workload
+    n_step = sum(t.n for t in tensors)
 
     descs = ws.nf4_tensors()
-    groups = [descs[i:i + _lib.NF4_MAX_BATCH] for i in range(0, len(descs), _lib.NF4_MAX_BATCH)]
-    carrs = [(_lib.TensorDesc * len(g))(*[d.c() for d in g]) for g in groups]
+    rep_carrs = []                          # per replica: its launches (<= NF4_MAX_BATCH tensors each)
+    for r in range(reps):
+        d = descs[r * nt:(r + 1) * nt]
+        groups = [d[i:i + _lib.NF4_MAX_BATCH] for i in range(0, len(d), _lib.NF4_MAX_BATCH)]
+        rep_carrs.append([(_lib.TensorDesc * len(g))(*[x.c() for x in g]) for g in groups])
+    carrs = rep_carrs[0]
     lib = nf4.load()
     odt = _lib.NF4_F16 if c.out_dtype == "f16" else _lib.NF4_BF16
     stream = torch.cuda.current_stream()
     sptr = stream.cuda_stream or None
     launch_events = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in carrs]
 
-    def step(timed_launches=None):
+    def step(timed_launches=None, i=0, s_ptr=None):
         n_launch = 0
-        for gi, arr in enumerate(carrs):
+        for gi, arr in enumerate(rep_carrs[i % reps]):
             if timed_launches is not None:
                 timed_launches[gi][0].record(stream)
-            st = lib.nf4_dequantize_batched(arr, len(arr), odt, sptr)
+            st = lib.nf4_dequantize_batched(arr, len(arr), odt, s_ptr or sptr)
             if st != 0:
                 raise _lib.NF4Error(st, "nf4_dequantize_batched")
             n_launch += lib.nf4_last_launch_count()
@@ -451,14 +473,17 @@ def measure_dequant(args, cfg, rank, world, device, nf4, torch, steps, full=True
                 timed_launches[gi][1].record(stream)
         return n_launch
 
-    for _ in range(args.warmup):
-        step()
+    for i in range(max(args.warmup, reps)):
+        step(i=i)
     torch.cuda.synchronize()
 
-    # Small (L2-resident) workloads: every timed step starts cold -- an L2 flush by
-    # READING 512 MB (a write-based flush would leave dirty lines whose write-back
-    # is charged to the step) runs between steps, outside the per-step events.
-    cold = ws.algorithmic_bytes() <= 8 * 126e6
+    # Small (L2-resident) workloads: `reps` rotating copies of the inputs and outputs
+    # (> 4 x L2 in total), and the timed steps -- step i on copy i % reps -- are
+    # launched back to back from ONE CUDA graph, so every step starts L2-cold and
+    # the time per step is the graph's time / steps (no per-launch event or
+    # host-launch floor).  The diagnostic per-launch pass below flushes L2 by
+    # READING 512 MB between single launches instead.
+    cold = reps > 1
     if cold:
         flush_buf = torch.ones(512 << 20, dtype=torch.uint8, device=device)
         flush_sink = torch.empty(1, dtype=torch.int64, device=device)
@@ -490,13 +515,17 @@ def measure_dequant(args, cfg, rank, world, device, nf4, torch, steps, full=True
     torch.cuda.synchronize()
     launches = 0
     if cold:
-        step_events = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                       for _ in range(steps)]
-        for s_ev, e_ev in step_events:
-            flush()
-            s_ev.record(stream)
-            launches += step()
-            e_ev.record(stream)
+        gs = torch.cuda.Stream(device=device)
+        gs.wait_stream(stream)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=gs):
+            for i in range(steps):
+                launches += step(i=i, s_ptr=gs.cuda_stream)
+        graph.replay()                       # warm-up replay (first replay uploads the graph)
+        torch.cuda.synchronize()
+        start.record(stream)
+        graph.replay()
+        end.record(stream)
     else:
         start.record(stream)
         for _ in range(steps):
@@ -506,15 +535,14 @@ def measure_dequant(args, cfg, rank, world, device, nf4, torch, steps, full=True
     if world > 1:
         dist.barrier()
     clocks = sampler.stop() if sampler else None
-    ms = sum(s_ev.elapsed_time(e_ev) for s_ev, e_ev in step_events) if cold else start.elapsed_time(end)
+    ms = start.elapsed_time(end)
     per_rank_ms = gather_per_rank(ms, device, world)
-    ms_max, tot_bytes, tot_elems = reduce_over_ranks(ms, float(ws.algorithmic_bytes()), float(ws.n_total),
-                                                     device, world)
+    ms_max, tot_bytes, tot_elems = reduce_over_ranks(ms, float(alg_step), float(n_step), device, world)
     value = tot_bytes * steps / (ms_max * 1e-3) / 1e9
     gelem = tot_elems * steps / (ms_max * 1e-3) / 1e9
     res = {"value": value, "gelem": gelem, "ms_max": ms_max, "ms_rank": ms, "per_rank_ms": per_rank_ms,
            "launches": launches, "launches_per_step": len(carrs), "kt": kt, "clocks": clocks, "cold": cold,
-           "t_build": t_build, "tensors": tensors, "alg_per_step": ws.algorithmic_bytes(), "n_rank": ws.n_total,
+           "reps": reps, "t_build": t_build, "tensors": tensors, "alg_per_step": alg_step, "n_rank": n_step,
            "tot_bytes": tot_bytes, "tot_elems": tot_elems}
     return res, ws
 
@@ -537,9 +565,13 @@ def f1_layer_groups(tensors):
 
 def measure_f1(nf4, torch, peak, ms_list=(1, 16, 64), layers=8, steps=20, warmup=5):
     """Y_t = X_t . W_t^T for every linear weight of `layers`
-    Gemma-3-27B decoder layers (DQ NF4, bf16 X/Y), fused (nf4_gemm_grouped for
-    the weights sharing X, nf4_gemm otherwise) vs the unfused path the paper
-    optimizes (nf4_dequantize into a bf16 buffer, then cuBLAS via torch.matmul).
+    Gemma-3-27B decoder layers (DQ NF4, bf16 X/Y), fused vs the unfused path the
+    paper optimizes (nf4_dequantize into a bf16 buffer, then cuBLAS via
+    torch.matmul).  Fused, two ways: `fused_ms` keeps a decoder layer's data
+    dependencies (q/k/v -> o -> gate/up -> down: one nf4_gemm_grouped launch for
+    the weights sharing X, nf4_gemm otherwise, 4 launches per layer);
+    `one_launch_ms` runs all the step's weights as independent problems in one
+    nf4_gemm_multi launch (fill/drain paid once).
     HBM roofline of the fused step: the bytes it must move (codes + qabsmax +
     absmax2 + X + Y) over the measured copy peak."""
     from synth import stores
@@ -578,6 +610,17 @@ def measure_f1(nf4, torch, peak, ms_list=(1, 16, 64), layers=8, steps=20, warmup
                     members = [(ws._ptr(ws.codes, ws.entries[i].codes_off), None, dqs[i], tensors[i].rows) for i in g]
                     nf4.nf4_gemm_grouped(xs[K], members, K=K, ys=[ys[i] for i in g], workspace=gws[tuple(g)])
 
+        mws = torch.zeros(max(16, nf4.nf4_gemm_multi_workspace_bytes(M, [t.rows for t in tensors],
+                                                                     [t.cols for t in tensors])),
+                          dtype=torch.uint8, device="cuda")
+        probs = [(xs[t.cols], t.cols, ws._ptr(ws.codes, e.codes_off), None, dqs[i], t.rows)
+                 for i, (t, e) in enumerate(zip(tensors, ws.entries))]
+
+        def one_launch():
+            # every weight of the step in ONE persistent launch (independent problems: the
+            # decode-step inputs are all ready, e.g. batched / speculative / MoE-style use)
+            nf4.nf4_gemm_multi(probs, M=M, ys=ys, workspace=mws)
+
         def unfused():
             for i, (t, e) in enumerate(zip(tensors, ws.entries)):
                 nf4.nf4_dequantize(ws._ptr(ws.codes, e.codes_off), None, dqs[i], n=e.n, blocksize=64,
@@ -597,6 +640,7 @@ def measure_f1(nf4, torch, peak, ms_list=(1, 16, 64), layers=8, steps=20, warmup
             return a.elapsed_time(b) / steps
 
         f_ms = timeit(fused)
+        o_ms = timeit(one_launch) if len(probs) <= 64 else None
         u_ms = timeit(unfused)
         wbytes = sum(e.n // 2 + e.n // 64 + 4 * (e.n // 64 // 256) for e in ws.entries) + 1024
         xybytes = sum(2 * M * (t.cols + t.rows) for t in tensors)
@@ -607,7 +651,13 @@ def measure_f1(nf4, torch, peak, ms_list=(1, 16, 64), layers=8, steps=20, warmup
                         "tflops": round(2.0 * M * n_total / (f_ms * 1e-3) / 1e12, 2),
                         "hbm_gbs": round(gbs, 1), "hbm_frac": round(gbs / peak, 4),
                         "bytes_per_step": wbytes + xybytes}
-        del xs, ys, gws
+        if o_ms is not None:
+            gbs1 = (wbytes + xybytes) / (o_ms * 1e-3) / 1e9
+            out[f"M{M}"].update({"one_launch_ms": round(o_ms, 4),
+                                 "one_launch_speedup_vs_dequant_plus_cublas": round(u_ms / o_ms, 3),
+                                 "one_launch_weights_per_s_T": round(n_total / (o_ms * 1e-3) / 1e12, 3),
+                                 "one_launch_hbm_frac": round(gbs1 / peak, 4)})
+        del xs, ys, gws, mws, probs
     del ws, wbuf
     torch.cuda.empty_cache()
     return out
@@ -673,7 +723,8 @@ def run_ours(args, rank, world, local_rank):
                                "roofline_frac": round(rx["value"] / peak, 4),
                                "pct_of_nominal_8000": round(100 * rx["value"] / NOMINAL_HBM_GBS, 2),
                                "bytes_per_step": rx["alg_per_step"], "launches_per_step": rx["launches_per_step"],
-                               "steps": max(10, args.steps // 2), "cold_l2": rx["cold"]}
+                               "steps": max(10, args.steps // 2), "cold_l2": rx["cold"],
+                               "rotating_copies": rx["reps"]}
 
     f1 = None
     if world == 1 and not args.no_f1:
@@ -702,8 +753,10 @@ def run_ours(args, rank, world, local_rank):
                        "algorithmic_bytes_per_step_total": int(r["tot_bytes"]),
                        "launches_per_step": r["launches_per_step"], "kernel_variant": variant,
                        "l2": "inputs+outputs per step >> 126 MB L2 (no flush needed)"
-                             if not r["cold"] else "L2 flushed (512 MB read) before every timed step; "
-                                                   "time = sum of per-step CUDA-event intervals",
+                             if not r["cold"] else f"L2-resident workload: {r['reps']} rotating copies "
+                                                   f"(> 4 x L2), the {args.steps} timed steps launched back to back "
+                                                   "from one CUDA graph (step i on copy i % copies); time = graph "
+                                                   "replay / steps",
                        "parallelism": (f"row-sharded {world} ways (each rank its own shard of every weight), "
                                        "no data-path collective" if args.scaling == "strong"
                                        else f"{world} independent replicas") if world > 1 else "single GPU"},
@@ -788,7 +841,7 @@ def main():
     ap.add_argument("--scaling", default="strong", choices=["weak", "strong"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--variant", default=None, help="dequant kernel variant (name or index)")
-    ap.add_argument("--extra-configs", default="cfg2", help="comma list measured after the main config (N=1)")
+    ap.add_argument("--extra-configs", default="cfg2,cfg1", help="comma list measured after the main config (N=1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sol", action="store_true")

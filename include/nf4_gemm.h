@@ -33,14 +33,20 @@
  *            buffer serves any sequence of calls on one stream (not two
  *            concurrent calls).  Results are deterministic for a given
  *            (splits, GPU).
+ *            The head of the workspace is a per-tile counter block that
+ *            classic calls never write (their fp32 partials start after it),
+ *            so classic and stream-K calls may share one buffer in any order.
  * Stream-ordered, asynchronous; status codes as nf4.h.
  * Programmatic dependent launch: the kernel may start while the previous
- * kernel on the stream drains, and it reads the WEIGHT (packed, absmax / dq
- * and its tables) before waiting for that kernel -- only x, y and the
- * workspace are ordered after it.  So the weight must not be written by the
- * immediately preceding kernel when that kernel triggers its dependents early
- * (none of this library's weight writers -- nf4_quantize,
- * nf4_double_quantize -- do; any other kernel triggers only at its exit).
+ * kernel on the stream drains.  By default it reads the WEIGHT (packed,
+ * absmax / dq and its tables) before waiting for that kernel -- only x, y and
+ * the workspace are ordered after it -- so a decode loop fetches and
+ * dequantizes the next weight while the previous kernel finishes.  CUDA only
+ * guarantees visibility of the previous kernel's writes after the wait, so a
+ * caller whose immediately preceding kernel WRITES the weight (an in-place
+ * update, a LoRA merge, a reload) must either call
+ * nf4_gemm_set_early_weight_reads(0) (every read after the wait; process-wide)
+ * or separate the two with an event / memcpy boundary.
  */
 #ifndef NF4_GEMM_H_
 #define NF4_GEMM_H_
@@ -85,6 +91,46 @@ nf4_status nf4_gemm_grouped(const void* x, nf4_dtype x_dtype, int32_t M, int32_t
                             const nf4_gemm_weight* weights, int32_t count, nf4_dtype y_dtype, void* workspace,
                             int64_t workspace_bytes, void* stream);
 int64_t nf4_gemm_grouped_workspace_bytes(int32_t M, const int32_t* N, int32_t count, int32_t K);
+
+/*
+ * Multi-problem form: up to NF4_GEMM_MAX_MULTI independent problems
+ * Y_i = X_i . W_i^T in ONE persistent stream-K launch -- every problem has its
+ * own activation X_i [M, K_i] and reduction length K_i; M, the X/Y dtypes and
+ * the blocksize are shared.  The problems' (tile, k-chunk) streams are
+ * concatenated problem by problem and cut into one equal range per SM, so the
+ * launch's fill and drain (~5-8 us) is paid once for all of them instead of
+ * once per GEMM -- e.g. every linear weight of several decoder layers at a
+ * decode step whose inputs are ready, or the experts of an MoE layer.
+ * Numerics are nf4_gemm's (bit-exact weights, fp32 accumulation; deterministic
+ * for a given problem list and GPU).
+ *   problems[i].x  [device] M x K_i, 16-byte aligned, x_dtype; may be shared.
+ *   problems[i].K  multiple of 64 and of blocksize (0: Y_i = 0).
+ *   others as nf4_gemm_weight.
+ * workspace: nf4_gemm_multi_workspace_bytes(M, N[], K[], count), zero-filled
+ * before first use and left zeroed (the stream-K contract of nf4_gemm).
+ * Errors: NF4_ERR_BAD_SIZE for count outside [1, NF4_GEMM_MAX_MULTI], a K that
+ * is not a multiple of 64 and of blocksize, or more than 2^31 chunk tiles in
+ * total; else as nf4_gemm.
+ */
+#define NF4_GEMM_MAX_MULTI 64
+typedef struct {
+  const void* x;           /* [device] M x K row-major, x_dtype */
+  int32_t K;
+  const uint8_t* packed;   /* [device] N*K/2 bytes, 16-byte aligned */
+  const float* absmax;     /* [device] fp32 absmax, or NULL for dq */
+  nf4_dq_state dq;         /* used when absmax == NULL */
+  int32_t N;
+  void* y;                 /* [device] M x N row-major, y_dtype */
+} nf4_gemm_problem;
+
+nf4_status nf4_gemm_multi(const nf4_gemm_problem* problems, int32_t count, int32_t M, nf4_dtype x_dtype,
+                          int32_t blocksize, nf4_dtype y_dtype, void* workspace, int64_t workspace_bytes,
+                          void* stream);
+int64_t nf4_gemm_multi_workspace_bytes(int32_t M, const int32_t* N, const int32_t* K, int32_t count);
+
+/* 1 (default): the GEMM kernels read the weight before griddepcontrol.wait
+ * (see above); 0: after it.  Process-wide, takes effect for later calls. */
+void nf4_gemm_set_early_weight_reads(int32_t enable);
 
 #ifdef __cplusplus
 }

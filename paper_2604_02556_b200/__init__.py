@@ -29,6 +29,7 @@ __all__ = [
     "nf4_dequantize_ex", "nf4_dequantize_batched_ex", "nf4_codebook_fp4",
     "nf4_gemm", "nf4_gemm_default_splits", "nf4_gemm_workspace_bytes", "nf4_dequantize_host_batched",
     "nf4_gemm_grouped", "nf4_gemm_grouped_workspace_bytes",
+    "nf4_gemm_multi", "nf4_gemm_multi_workspace_bytes", "nf4_gemm_set_early_weight_reads",
 ]
 
 
@@ -345,3 +346,53 @@ def nf4_gemm_grouped(x, weights, *, K: int, blocksize: int = 64, ys=None, y_dtyp
                                  ycode, _ptr(workspace), int(wsize), _stream(stream))
     _lib.check(st, "nf4_gemm_grouped")
     return ys
+
+
+def nf4_gemm_multi_workspace_bytes(M: int, Ns, Ks) -> int:
+    Ns, Ks = tuple(int(n) for n in Ns), tuple(int(k) for k in Ks)
+    return _multi_ws_bytes(int(M), Ns, Ks)
+
+
+@functools.lru_cache(maxsize=4096)
+def _multi_ws_bytes(M: int, Ns: tuple, Ks: tuple) -> int:
+    na = (ctypes.c_int32 * len(Ns))(*Ns)
+    ka = (ctypes.c_int32 * len(Ks))(*Ks)
+    return int(load().nf4_gemm_multi_workspace_bytes(M, na, ka, len(Ns)))
+
+
+def nf4_gemm_multi(problems, *, M: int, blocksize: int = 64, x_dtype="bf16", y_dtype="bf16", ys=None,
+                   workspace=None, stream=None):
+    """Y_i = X_i . W_i^T for up to NF4_GEMM_MAX_MULTI independent problems in ONE
+    persistent stream-K launch (include/nf4_gemm.h).  problems: sequence of
+    (x [M, K_i], K_i, packed, absmax, dq, N_i).  Returns the list of y_i [M, N_i]
+    (allocated with torch unless `ys` is given)."""
+    import torch
+    ycode = _dtype_code(y_dtype)
+    tdt = {_lib.NF4_F16: torch.float16, _lib.NF4_BF16: torch.bfloat16, _lib.NF4_F32: torch.float32}[ycode]
+    if ys is None:
+        dev = next((q[0].device for q in problems if hasattr(q[0], "device")), None)
+        ys = [torch.empty((M, int(q[5])), dtype=tdt, device=dev) for q in problems]
+    Ns = tuple(int(q[5]) for q in problems)
+    Ks = tuple(int(q[1]) for q in problems)
+    wbytes = _multi_ws_bytes(int(M), Ns, Ks)
+    if wbytes > 0 and workspace is None:
+        workspace = torch.zeros(wbytes, dtype=torch.uint8, device=ys[0].device)
+    wsize = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    arr = (_lib.GemmProblem * len(problems))()
+    for i, (x, K, packed, absmax, dq, n) in enumerate(problems):
+        arr[i].x = _ptr(x)
+        arr[i].K = int(K)
+        arr[i].packed = _ptr(packed)
+        arr[i].absmax = _ptr(absmax)
+        if dq is not None:
+            arr[i].dq = dq.c()
+        arr[i].N = int(n)
+        arr[i].y = _ptr(ys[i])
+    st = load().nf4_gemm_multi(arr, len(problems), int(M), _dtype_code(x_dtype), int(blocksize), ycode,
+                               _ptr(workspace), int(wsize), _stream(stream))
+    _lib.check(st, "nf4_gemm_multi")
+    return ys
+
+
+def nf4_gemm_set_early_weight_reads(enable: bool) -> None:
+    load().nf4_gemm_set_early_weight_reads(1 if enable else 0)

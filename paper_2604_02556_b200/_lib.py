@@ -33,6 +33,7 @@ EXPORTS = [
     "nf4_dequantize_ex", "nf4_dequantize_batched_ex", "nf4_codebook_fp4",
     "nf4_gemm", "nf4_gemm_default_splits", "nf4_gemm_workspace_bytes", "nf4_dequantize_host_batched",
     "nf4_gemm_grouped", "nf4_gemm_grouped_workspace_bytes",
+    "nf4_gemm_multi", "nf4_gemm_multi_workspace_bytes", "nf4_gemm_set_early_weight_reads",
 ]
 
 
@@ -49,6 +50,13 @@ class GemmWeight(ctypes.Structure):
 
 
 NF4_GEMM_MAX_GROUP = 4
+NF4_GEMM_MAX_MULTI = 64
+
+
+class GemmProblem(ctypes.Structure):
+    """nf4_gemm_problem"""
+    _fields_ = [("x", ctypes.c_void_p), ("K", ctypes.c_int32), ("packed", ctypes.c_void_p),
+                ("absmax", ctypes.c_void_p), ("dq", DQState), ("N", ctypes.c_int32), ("y", ctypes.c_void_p)]
 
 
 class TensorDesc(ctypes.Structure):
@@ -95,6 +103,10 @@ def load() -> ctypes.CDLL:
             "nf4_gemm_workspace_bytes": ([i32, i32, i32, i32], i64),
             "nf4_gemm_grouped": ([P, i32, i32, i32, i32, ctypes.POINTER(GemmWeight), i32, i32, P, i64, P], st),
             "nf4_gemm_grouped_workspace_bytes": ([i32, ctypes.POINTER(ctypes.c_int32), i32, i32], i64),
+            "nf4_gemm_multi": ([ctypes.POINTER(GemmProblem), i32, i32, i32, i32, i32, P, i64, P], st),
+            "nf4_gemm_multi_workspace_bytes": ([i32, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
+                                                i32], i64),
+            "nf4_gemm_set_early_weight_reads": ([i32], None),
             "nf4_dequantize_ex": ([P, P, ctypes.POINTER(DQState), i64, i32, P, i32, P, P], st),
             "nf4_dequantize_batched_ex": ([ctypes.POINTER(TensorDesc), i32, P, i32, P], st),
             "nf4_status_string": ([st], ctypes.c_char_p),

@@ -50,11 +50,8 @@ namespace gemm {
 // 2-chunk super-stages x 10, 5 x 2 A tiles in TMEM): more, smaller hand-offs, so a
 // group that ran ahead waits less for the in-order MMA.  Wider tiles keep 3 groups
 // of 8 warps (2 threads per row), whose 4-chunk stages suit the heavier MMA/X side.
-// DQ second-level table: read through L1 from global memory (no prologue staging,
-// whose global round trip sat before the block-wide sync) instead of from smem.
-#ifndef NF4_GEMM_CODE2_GLOBAL
-#define NF4_GEMM_CODE2_GLOBAL 1   // 1: -4% at M=1, -1% at M=128 (grouped 8-layer step)
-#endif
+// DQ second-level table (code2): read through L1 from global memory (staging it in
+// shared memory put a global round trip before the block-wide sync: +4% at M=1).
 #ifndef NF4_GEMM_W4_MAXBN
 #define NF4_GEMM_W4_MAXBN 16
 #endif
@@ -65,17 +62,29 @@ namespace gemm {
 #define NF4_GEMM_W4_GROUPS 5
 #endif
 #ifndef NF4_GEMM_W4_CST
-#define NF4_GEMM_W4_CST 10
+#define NF4_GEMM_W4_CST 12
+#endif
+// A-tile slots in TMEM for 4-warp groups (BN = 16): more slots than groups let a
+// group that ran ahead start its next super-stage before the in-order MMA has
+// consumed its previous one (it waits only for the slot's previous occupant).
+// TMEM: NACC x 32 accumulator columns + SLOTS x SUB x 32 A columns <= 512.
+#ifndef NF4_GEMM_W4_SLOTS
+#define NF4_GEMM_W4_SLOTS 7
 #endif
 template <int BN> __host__ __device__ constexpr int wpg_for() { return BN <= NF4_GEMM_W4_MAXBN ? 4 : 8; }
 template <int BN> __host__ __device__ constexpr int groups_for() { return BN <= NF4_GEMM_W4_MAXBN ? NF4_GEMM_W4_GROUPS : NF4_GEMM_GROUPS; }
+template <int BN> __host__ __device__ constexpr int slots_for() { return BN <= NF4_GEMM_W4_MAXBN ? NF4_GEMM_W4_SLOTS : groups_for<BN>(); }
 constexpr int kCodeBytes = 32;              // packed bytes per row per k-chunk
 constexpr int kChunk = 64;          // k elements per stage (= one 128 B swizzle row in 16-bit)
 constexpr int kRowBytes = 128;
 
-// One weight of a (grouped) GEMM: all members share X, K and the blocksize; their
-// output-feature tiles are concatenated into one tile stream.
-constexpr int kMaxMembers = 4;
+// One weight (problem) of a multi-weight launch.  nf4_gemm_grouped: members share
+// X and K; nf4_gemm_multi: every member has its own X and K (M and the blocksize
+// are shared).  Work order is member-major: member g owns the global chunks
+// [cbase, cbase + tiles_n * tiles_m * nk) and the global 128-feature tiles
+// [tile0, tile0 + tiles_n) (partial-sum columns) and [ftile0, ftile0 + tiles_n *
+// tiles_m) (stream-K counters).
+constexpr int kMaxMembers = 64;
 struct Member {
   const float* absmax;     // fp32 mode if non-null
   const uint8_t* qabsmax;  // DQ mode
@@ -84,35 +93,41 @@ struct Member {
   void* y;                 // [M, N] row-major
   float offset;
   int32_t N;
-  int32_t tile0;           // first (global) 128-feature tile of this member
+  int32_t K, nk;           // reduction length and its 64-element chunks
+  int32_t tiles_n;         // 128-feature tiles of this member
+  int32_t tile0;           // first global 128-feature tile (partial-sum column block)
+  int32_t ftile0;          // first global tile (stream-K counter)
+  int32_t cbase;           // first global chunk
 };
 template <int NM>
-struct CodeMapsT {         // one TMA descriptor per member's packed codes
-  CUtensorMap m[NM];
+struct MapsT {             // TMA descriptors per member: packed codes, X
+  CUtensorMap c[NM];
+  CUtensorMap x[NM];
 };
-using CodeMaps = CodeMapsT<kMaxMembers>;
 
-struct GemmParams {
-  Member mem[kMaxMembers];
+struct GemmCommon {
   int32_t nmem;
-  const uint16_t* x;       // [M, K] 16-bit
   float* partial;          // [splits, M, Npad] fp32 (classic) / [parts, M, Npad] (stream-K)
   unsigned* flags;         // stream-K: per-tile count of published partials (zero between calls)
-  int32_t M, K;
-  int32_t Npad;            // tiles_n * 128: row stride of the partials
+  int32_t M;
+  int32_t Npad;            // (sum of tiles_n) * 128: row stride of the partials
   int32_t bs_shift;
   int32_t chunks_per_split;  // classic split-K
   int32_t splits;            // classic split-K (1 = direct output)
   int32_t out_dtype;         // NF4_F16 / NF4_BF16 / NF4_F32
   int32_t streamk;           // 1: stream-K ranges over a 1-D grid
-  int32_t tiles_n, tiles_m;  // tile grid (128 features x BN tokens), tiles_n over all members
-  int32_t nk;                // 64-element chunks per tile (K / 64)
-  int64_t total_chunks;      // tiles_n * tiles_m * nk
+  int32_t tiles_m;           // token tiles (BN tokens each)
+  int64_t total_chunks;      // all members
   int32_t align4;            // stream-K range bounds rounded to 4 chunks
+  int32_t early_weights;     // 1: read the weight before griddepcontrol.wait (nf4_gemm.h)
   unsigned long long* trace;  // diagnostics only (NF4_GEMM_TRACE): per-CTA start / end / SM / last epilogue
   int32_t experiment;         // diagnostics only (NF4_GEMM_EXPERIMENT): 1 skip MMA, 2 skip dequant, 4 skip tcgen05.st,
                               // 8 skip X loads, 16 skip code loads
   float lut[16];
+};
+template <int NM>
+struct GemmParamsT : GemmCommon {
+  Member mem[NM];
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -237,20 +252,42 @@ __host__ __device__ __forceinline__ int64_t sk_owner(int64_t x, int64_t W, int64
   return c;
 }
 
-__device__ __forceinline__ int member_of(const GemmParams& p, int tn) {
-  int g = 0;
-#pragma unroll
-  for (int i = 1; i < kMaxMembers; ++i)
-    if (i < p.nmem && tn >= p.mem[i].tile0) g = i;
-  return g;
+// Member owning global chunk x (binary search over the members' first chunks).
+template <int NM>
+__device__ __forceinline__ int member_of_chunk(const GemmParamsT<NM>& p, int x) {
+  if constexpr (NM == 1) {
+    return 0;
+  } else {
+    int lo = 0, hi = p.nmem - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (p.mem[mid].cbase <= x) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+  }
+}
+// The tile containing global chunk x: member g, member-local tile tl, its first chunk and length.
+struct TileAt {
+  int g, tl, tstart, nkt;
+};
+template <int NM>
+__device__ __forceinline__ TileAt tile_at(const GemmParamsT<NM>& p, int x) {
+  TileAt t;
+  t.g = member_of_chunk(p, x);
+  t.nkt = p.mem[t.g].nk;
+  t.tl = (x - p.mem[t.g].cbase) / t.nkt;
+  t.tstart = p.mem[t.g].cbase + t.tl * t.nkt;
+  return t;
 }
 
 // One segment = a contiguous k-range of one output tile processed by one CTA.
 struct Segment {
   int g;          // member
-  int tn;         // global 128-feature tile index (partials, counters)
+  int tn;         // global 128-feature tile index (partial-sum columns)
+  int ft;         // global tile index (stream-K counter)
   int n0, m0;     // tile origin (member-local features, tokens)
   int kc0, nk;    // first chunk within the tile, chunk count
+  int nkt;        // chunks of the whole tile (the member's K / 64)
   int part;       // partial-sum slot (stream-K: segment index within the tile; classic: split)
 };
 
@@ -309,17 +346,19 @@ struct SegIter {
   int phase;           // 0: head piece, 1: the rest
   int done_classic;
 };
-template <int BN, bool MULTI>
-__device__ __forceinline__ bool next_segment(const GemmParams& p, SegIter& it, Segment& sg) {
+template <int BN, int NM>
+__device__ __forceinline__ bool next_segment(const GemmParamsT<NM>& p, SegIter& it, Segment& sg) {
   if (!p.streamk) {
     if (it.done_classic) return false;
     it.done_classic = 1;
     sg.g = 0;
     sg.tn = blockIdx.x;
+    sg.ft = blockIdx.x + blockIdx.y * p.mem[0].tiles_n;
     sg.n0 = blockIdx.x * 128;
     sg.m0 = blockIdx.y * BN;
+    sg.nkt = p.mem[0].nk;
     sg.kc0 = blockIdx.z * p.chunks_per_split;
-    const int kc1 = min(p.nk, sg.kc0 + p.chunks_per_split);
+    const int kc1 = min(sg.nkt, sg.kc0 + p.chunks_per_split);
     sg.nk = kc1 > sg.kc0 ? kc1 - sg.kc0 : 0;
     sg.part = blockIdx.z;
     return true;
@@ -330,20 +369,24 @@ __device__ __forceinline__ bool next_segment(const GemmParams& p, SegIter& it, S
     it.x = it.start;
     it.end = it.hs;
   }
-  const int tile = it.x / p.nk;
-  const int tstart = tile * p.nk;
-  const int send = min(it.end, tstart + p.nk);
-  sg.tn = tile % p.tiles_n;
-  sg.g = MULTI ? member_of(p, sg.tn) : 0;   // single weight: member 0 (constant-bank operands)
-  sg.n0 = (sg.tn - p.mem[sg.g].tile0) * 128;
-  sg.m0 = (tile / p.tiles_n) * BN;
-  sg.kc0 = it.x - tstart;
+  const TileAt t = tile_at(p, it.x);   // single weight: member 0 (constant-bank operands)
+  const int send = min(it.end, t.tstart + t.nkt);
+  const int tiles_n = p.mem[t.g].tiles_n;
+  const int tn = t.tl % tiles_n;
+  sg.g = t.g;
+  sg.tn = p.mem[t.g].tile0 + tn;
+  sg.ft = p.mem[t.g].ftile0 + t.tl;
+  sg.n0 = tn * 128;
+  sg.m0 = (t.tl / tiles_n) * BN;
+  sg.nkt = t.nkt;
+  sg.kc0 = it.x - t.tstart;
   sg.nk = send - it.x;
   sg.part = it.x == it.start ? it.part0 : 0;
   it.x = send;
   return true;
 }
-__device__ __forceinline__ SegIter seg_begin(const GemmParams& p, const int (&range)[3]) {
+template <int NM>
+__device__ __forceinline__ SegIter seg_begin(const GemmParamsT<NM>& p, const int (&range)[3]) {
   SegIter it;
   it.done_classic = 0;
   it.start = range[0];
@@ -353,11 +396,11 @@ __device__ __forceinline__ SegIter seg_begin(const GemmParams& p, const int (&ra
   it.x = range[0];
   it.end = range[1];
   if (p.streamk && range[1] > range[0]) {
-    const int tl = (range[1] - 1) / p.nk, tsl = tl * p.nk;
-    if (range[1] < tsl + p.nk && tsl > range[0]) {   // the range ends inside a tile it did not start in
-      it.hs = tsl;
+    const TileAt t = tile_at(p, range[1] - 1);
+    if (range[1] < t.tstart + t.nkt && t.tstart > range[0]) {   // the range ends inside a tile it did not start in
+      it.hs = t.tstart;
       it.phase = 0;
-      it.x = tsl;                                      // head piece [tsl, end) first
+      it.x = t.tstart;                                          // head piece [tstart, end) first
     }
   }
   return it;
@@ -399,25 +442,26 @@ struct Scales {
 // piece order at the end of its range and writes y.  It waits only for
 // lower-numbered CTAs, dispatched before it, which compute the head piece of
 // their last tile first (seg_begin), so the wait is normally already over.
-// Grouped GEMMs (MULTI): the segment's member selects the TMA descriptor,
+// Grouped / multi-problem GEMMs (NM > 1): the segment's member selects the TMA descriptors,
 // scale pointers, code2 table and output.
-template <int BN, int G, int SUB, int CST, int NACC, bool BF16, bool MULTI>
+template <int BN, int G, int SUB, int CST, int NACC, bool BF16, int NM>
 __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
-    nf4_gemm_kernel(const __grid_constant__ GemmParams p, const __grid_constant__ CodeMapsT<MULTI ? kMaxMembers : 1> maps,
-                    const __grid_constant__ CUtensorMap map_x) {
-  constexpr int kMem = MULTI ? kMaxMembers : 1;   // members this instantiation serves
+    nf4_gemm_kernel(const __grid_constant__ GemmParamsT<NM> p, const __grid_constant__ MapsT<NM> maps) {
+  // NM: members this instantiation serves (1, NF4_GEMM_MAX_GROUP or kMaxMembers: the
+  // parameter block is copied at every launch, so small groups use a small one)
   static_assert(CST >= G, "a super-stage slot must not be two phases behind any group");
   constexpr int kProducerWarps = wpg_for<BN>();
   constexpr int kMmaWarp = kProducerWarps * G, kTmaWarp = kProducerWarps * G + 1;
   constexpr int ACC = BN < 32 ? 32 : BN;
   constexpr int A0 = NACC * ACC;
-  static_assert(A0 + G * SUB * 32 <= 512, "TMEM budget");
+  constexpr int S = slots_for<BN>();   // A-tile slots: super-stage Jg uses slot Jg % S
+  static_assert(S >= G, "a group's previous fill must have freed the slot's previous-but-one use");
+  static_assert(A0 + S * SUB * 32 <= 512, "TMEM budget");
   constexpr int kSuperCodeBytes = 128 * SUB * kCodeBytes;
   constexpr int kSuperXBytes = SUB * BN * kRowBytes;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ __align__(256) float lut[16];                    // 256-B aligned: address = PRMT(offsets, base)
-  __shared__ float code2s[kMem][NF4_GEMM_CODE2_GLOBAL ? 1 : 256];   // DQ second-level tables (staged variant)
-  __shared__ __align__(8) uint64_t c_full[CST], x_full[CST], c_free[CST], w_full[G], a_free[G], acc_full[NACC],
+  __shared__ __align__(8) uint64_t c_full[CST], x_full[CST], c_free[CST], w_full[S], a_free[S], acc_full[NACC],
       acc_empty[NACC];
   __shared__ uint32_t tmem_holder;
   __shared__ int sk_range[3];                                 // stream-K: range start, end, first slot
@@ -450,7 +494,7 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
       mbar_init(&x_full[s], 1);
       mbar_init(&c_free[s], 1);
     }
-    for (int s = 0; s < G; ++s) {
+    for (int s = 0; s < S; ++s) {
       mbar_init(&w_full[s], kProducerWarps);
       mbar_init(&a_free[s], 1);
     }
@@ -464,7 +508,7 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
       const int64_t x0 = sk_bound(blockIdx.x, W, NG, p.align4);
       sk_range[0] = int(x0);
       sk_range[1] = int(sk_bound(blockIdx.x + 1, W, NG, p.align4));
-      sk_range[2] = int(blockIdx.x - sk_owner(x0 / p.nk * p.nk, W, NG, p.align4));
+      sk_range[2] = x0 < W ? int(blockIdx.x - sk_owner(tile_at(p, int(x0)).tstart, W, NG, p.align4)) : 0;
     } else {
       sk_range[0] = sk_range[1] = sk_range[2] = 0;
     }
@@ -475,9 +519,10 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   if (warp == kTmaWarp && lane == 0) {
-    for (int i = 0; i < kMem && i < p.nmem; ++i)
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.m[i])) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_x)) : "memory");
+    for (int i = 0; i < NM && i < p.nmem && i < 8; ++i) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.c[i])) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.x[i])) : "memory");
+    }
   }
   // Programmatic dependent launch: the next kernel in the stream may start its own
   // prologue as soon as our CTAs leave their SMs.  Only X, y and the workspace
@@ -488,15 +533,12 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
   // waits before loading X, the producers before their first store to y or
   // the workspace, everybody before the stream-K fix-up.
   if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  for (int i = 0; i < kMem && i < p.nmem; ++i) {
-    if (p.mem[i].absmax == nullptr)
-      if (!NF4_GEMM_CODE2_GLOBAL)
-        for (int t = threadIdx.x; t < 256; t += blockDim.x) code2s[i][t] = p.mem[i].code2[t];
-  }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_holder;
+  // weights written by the immediately preceding kernel: read nothing before it completes
+  if (!p.early_weights) asm volatile("griddepcontrol.wait;" ::: "memory");
   if (NF4_TRACING && cta_lin == 0 && threadIdx.x == 0) p.trace[0] = gtimer();
 
   if (warp < kProducerWarps * G) {
@@ -512,18 +554,19 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
     int J = 0, sidx = 0;                       // super-stages / segments before this segment
     SegIter it = seg_begin(p, sk_range);
     Segment sg;
-    while (next_segment<BN, MULTI>(p, it, sg)) {
+    while (next_segment<BN>(p, it, sg)) {
       // this segment's weight (member of a grouped GEMM)
       // (read from the parameter bank at each use: keeping them in registers spilled)
 #define absmax (p.mem[sg.g].absmax)
 #define qabsmax (p.mem[sg.g].qabsmax)
 #define absmax2 (p.mem[sg.g].absmax2)
       const float offset = p.mem[sg.g].offset;
-      const float* c2 = NF4_GEMM_CODE2_GLOBAL ? p.mem[sg.g].code2 : code2s[sg.g];
+      const float* c2 = p.mem[sg.g].code2;
       const int Nm = p.mem[sg.g].N;
+      const int Km = p.mem[sg.g].K;
       const int row = sg.n0 + t;
       const bool row_ok = row < Nm;
-      const int64_t blk_base = (int64_t(row) * p.K) >> p.bs_shift;
+      const int64_t blk_base = (int64_t(row) * Km) >> p.bs_shift;
       const int nk = sg.nk, kc0 = sg.kc0;
       const int nsuper = (nk + SUB - 1) / SUB;
       // fast: blocksize 64 and whole, aligned super-stages -- the SUB scales of a
@@ -531,7 +574,7 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
       // consecutive qabsmax bytes (one load) plus the 1-2 absmax2 groups they span
       // (2-chunk stages: BN = 64 only -- 0.5% slower at BN = 128, measured)
       const bool fast =
-          (SUB == 4 || (SUB == 2 && BN <= 64)) && p.bs_shift == 6 && (p.K % (64 * SUB)) == 0 && (kc0 % SUB) == 0 &&
+          (SUB == 4 || (SUB == 2 && BN <= 64)) && p.bs_shift == 6 && (Km % (64 * SUB)) == 0 && (kc0 % SUB) == 0 &&
           (nk % SUB) == 0 &&
           (absmax != nullptr ? (reinterpret_cast<uintptr_t>(absmax) & (4 * SUB - 1)) == 0
                                : (reinterpret_cast<uintptr_t>(qabsmax) & (SUB - 1)) == 0);
@@ -581,7 +624,8 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
         if (j + G < nsuper) fetch(nxt, j + G);   // one super-stage ahead (hides the L2 latency)
         const int Jg = J + j;
         const int cs = Jg % CST;
-        const uint32_t aph = uint32_t(Jg / G) & 1u;
+        const int slot = Jg % S;
+        const uint32_t aph = uint32_t(Jg / S) & 1u;
         mbar_wait_parity(&c_full[cs], uint32_t(Jg / CST) & 1u);   // codes of this super-stage landed
         if (wl == 0 && lane == 0) NF4_TRACE_J(100, Jg);
         const int64_t b0 = blk_base + kc0 + SUB * j;
@@ -602,9 +646,9 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
               // A4 (R7): fl32(fl32(code2[qabsmax] * absmax2) + offset), two roundings
               const uint32_t qb = (sc.s[0] >> (8 * q)) & 0xFFu;
               const float a2 = ((b0 + q) >> 8) == (b0 >> 8) ? sc.a2[0] : sc.a2[1];
-              a = __fadd_rn(__fmul_rn(NF4_GEMM_CODE2_GLOBAL ? __ldg(c2 + qb) : c2[qb], a2), offset);
+              a = __fadd_rn(__fmul_rn(__ldg(c2 + qb), a2), offset);
             } else {
-              a = __fadd_rn(__fmul_rn(NF4_GEMM_CODE2_GLOBAL ? __ldg(c2 + sc.s[q]) : c2[sc.s[q]], sc.a2[q]), offset);
+              a = __fadd_rn(__fmul_rn(__ldg(c2 + sc.s[q]), sc.a2[q]), offset);
             }
             const uint64_t aa = f32x2_splat(a);
             // 8-warp groups: this thread's half of the chunk; 4-warp groups: both halves
@@ -638,12 +682,12 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
                   constexpr int kWords = 16 / (NF4_GEMM_ST_SPLIT ? NF4_GEMM_ST_SPLIT : 1), kCc = kWords / 4;
                   if (cc % kCc == kCc - 1) {
                     if (first && cc == kCc - 1) {
-                      mbar_wait_parity(&a_free[g], aph ^ 1u);        // the MMA is done with our previous A tiles
+                      mbar_wait_parity(&a_free[slot], aph ^ 1u);        // the MMA is done with our previous A tiles
                       if (wl == 0 && lane == 0) NF4_TRACE_J(200, Jg);
                       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     }
                     const int w0 = (cc / kCc) * kWords;
-                    const uint32_t taddr = tmem + tlane + uint32_t(A0 + (g * SUB + q) * 32 + hh * 16 + w0);
+                    const uint32_t taddr = tmem + tlane + uint32_t(A0 + (slot * SUB + q) * 32 + hh * 16 + w0);
                     if (!NF4_EXP(4)) {
                       if constexpr (kWords == 8)
                         asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
@@ -690,13 +734,13 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
                   }
                 }
                 if (first) {
-                  mbar_wait_parity(&a_free[g], aph ^ 1u);              // the MMA is done with our previous A tiles
+                  mbar_wait_parity(&a_free[slot], aph ^ 1u);              // the MMA is done with our previous A tiles
                   if (wl == 0 && lane == 0) NF4_TRACE_J(200, Jg);
                   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 }
                 if (!NF4_EXP(4)) {
                   // 16 columns (32 weights) of this row's A tile (group g, chunk q) in TMEM
-                  const uint32_t taddr = tmem + tlane + uint32_t(A0 + (g * SUB + q) * 32 + hh * 16);
+                  const uint32_t taddr = tmem + tlane + uint32_t(A0 + (slot * SUB + q) * 32 + hh * 16);
                   asm volatile(
                       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
                       ::"r"(taddr), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]),
@@ -721,7 +765,7 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
         if (wl == 0 && lane == 0) NF4_TRACE_J(300, Jg);
-        if (lane == 0) mbar_arrive(&w_full[g]);      // A tiles written, codes read
+        if (lane == 0) mbar_arrive(&w_full[slot]);   // A tiles written, codes read
       }
 
       // ======================= epilogue (the group of the segment's last super-stage) =======================
@@ -737,7 +781,7 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
         const int col0 = half * HB;
         const int n = sg.n0 + qd * 32 + lane;
         const uint32_t taddr = tmem + (uint32_t(qd * 32) << 16) + uint32_t(ab * ACC);
-        const bool direct = p.streamk ? (sg.kc0 == 0 && nk == p.nk) : p.splits == 1;
+        const bool direct = p.streamk ? (sg.kc0 == 0 && nk == sg.nkt) : p.splits == 1;
         void* ym = p.mem[sg.g].y;
 #pragma unroll 1
         for (int cb = col0; cb < col0 + HB && cb < BN; cb += 16) {
@@ -769,11 +813,11 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_empty[ab]);     // the MMA may reuse this accumulator
-        if (p.streamk && !direct && sg.kc0 + nk < p.nk) {
+        if (p.streamk && !direct && sg.kc0 + nk < sg.nkt) {
           // a non-final piece: publish (release) -- the tile's last CTA sums it at its end
           __threadfence();
           __syncwarp();
-          if (lane == 0) atomicAdd(p.flags + (sg.m0 / BN) * p.tiles_n + sg.tn, 1u);
+          if (lane == 0) atomicAdd(p.flags + sg.ft, 1u);
         }
         if (NF4_TRACING && wl == 0 && lane == 0) p.trace[1024 + 4 * cta_lin + 3] = gtimer();
       }
@@ -793,13 +837,13 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
       auto issue_codes = [&](const Segment& sg, int j, int cs) {
         asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&c_full[cs])),
                      "r"(uint32_t(ld_c ? kSuperCodeBytes : 0)) : "memory");
-        if (ld_c) tma_load_2d(smem_c + cs * kSuperCodeBytes, &maps.m[sg.g], (sg.kc0 + j * SUB) * kChunk / 2, sg.n0,
+        if (ld_c) tma_load_2d(smem_c + cs * kSuperCodeBytes, &maps.c[sg.g], (sg.kc0 + j * SUB) * kChunk / 2, sg.n0,
                               &c_full[cs]);
       };
       int J = 0;
       SegIter it = seg_begin(p, sk_range);
       Segment sg;
-      while (J < CST && next_segment<BN, MULTI>(p, it, sg)) {
+      while (J < CST && next_segment<BN>(p, it, sg)) {
         const int nsuper = (sg.nk + SUB - 1) / SUB;
         for (int j = 0; j < nsuper && J + j < CST; ++j) issue_codes(sg, j, J + j);
         J += nsuper;
@@ -807,7 +851,7 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
       asm volatile("griddepcontrol.wait;" ::: "memory");   // X is the previous kernel's output
       J = 0;
       it = seg_begin(p, sk_range);
-      while (next_segment<BN, MULTI>(p, it, sg)) {
+      while (next_segment<BN>(p, it, sg)) {
         const int nsuper = (sg.nk + SUB - 1) / SUB;
         for (int j = 0; j < nsuper; ++j) {
           const int Jg = J + j, cs = Jg % CST;
@@ -822,7 +866,7 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
           if (ld_x) {
 #pragma unroll
             for (int q = 0; q < SUB; ++q)
-              tma_load_2d(smem_x + cs * kSuperXBytes + q * BN * kRowBytes, &map_x, k0 + q * kChunk, sg.m0,
+              tma_load_2d(smem_x + cs * kSuperXBytes + q * BN * kRowBytes, &maps.x[sg.g], k0 + q * kChunk, sg.m0,
                           &x_full[cs]);
           }
         }
@@ -835,21 +879,21 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
     int J = 0, sidx = 0;
     SegIter it = seg_begin(p, sk_range);
     Segment sg;
-    while (next_segment<BN, MULTI>(p, it, sg)) {
+    while (next_segment<BN>(p, it, sg)) {
       const int nsuper = (sg.nk + SUB - 1) / SUB;
       const int ab = sidx % NACC;
       mbar_wait_parity(&acc_empty[ab], (uint32_t(sidx / NACC) & 1u) ^ 1u);   // its previous epilogue done
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t d_tmem = tmem + uint32_t(ab * ACC);
       for (int j = 0; j < nsuper; ++j) {
-        const int Jg = J + j, g = Jg % G, cs = Jg % CST;
-        mbar_wait_parity(&w_full[g], uint32_t(Jg / G) & 1u);               // A tiles in TMEM
+        const int Jg = J + j, slot = Jg % S, cs = Jg % CST;
+        mbar_wait_parity(&w_full[slot], uint32_t(Jg / S) & 1u);            // A tiles in TMEM
         mbar_wait_parity(&x_full[cs], uint32_t(Jg / CST) & 1u);            // X of this super-stage landed
         if (lane == 0) NF4_TRACE_J(500, Jg);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if (!(NF4_EXP(1))) {
           const uint64_t b0 = umma_desc_sw128(smem_u32(smem_x + cs * kSuperXBytes));
-          const uint32_t a0 = tmem + uint32_t(A0 + g * SUB * 32);
+          const uint32_t a0 = tmem + uint32_t(A0 + slot * SUB * 32);
 #pragma unroll
           for (int q = 0; q < SUB; ++q) {
             if (j * SUB + q < sg.nk)
@@ -857,7 +901,7 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
                                (j > 0 || q > 0) ? 1u : 0u);
           }
         }
-        umma_commit_elect(&a_free[g]);
+        umma_commit_elect(&a_free[slot]);
         umma_commit_elect(&c_free[cs]);
       }
       if (nsuper > 0)
@@ -874,9 +918,11 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
   __syncthreads();
   if (p.streamk) {
     // ======================= stream-K fix-up of the tile this range finishes =======================
-    const int x0 = sk_range[0], tile = x0 / p.nk, kc0 = x0 - tile * p.nk, parts = sk_range[2] + 1;
-    if (kc0 > 0 && sk_range[1] >= (tile + 1) * p.nk) {
-      unsigned* flag = p.flags + tile;
+    const int x0 = sk_range[0], parts = sk_range[2] + 1;
+    const TileAt t = tile_at(p, x0 < p.total_chunks ? x0 : 0);
+    const int kc0 = x0 - t.tstart;
+    if (x0 < sk_range[1] && kc0 > 0 && sk_range[1] >= t.tstart + t.nkt) {
+      unsigned* flag = p.flags + p.mem[t.g].ftile0 + t.tl;
       if (threadIdx.x == 0) {
         const unsigned want = unsigned(kProducerWarps * (parts - 1));
         unsigned v;
@@ -888,8 +934,9 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
         *flag = 0u;                                   // leave the workspace clean for the next call
       }
       __syncthreads();
-      const int tn = tile % p.tiles_n, gm = MULTI ? member_of(p, tn) : 0;
-      const int n0 = (tn - p.mem[gm].tile0) * 128, m0 = (tile / p.tiles_n) * BN;
+      const int gm = t.g, tiles_n = p.mem[gm].tiles_n;
+      const int tn = p.mem[gm].tile0 + t.tl % tiles_n;
+      const int n0 = (t.tl % tiles_n) * 128, m0 = (t.tl / tiles_n) * BN;
       const int Nm = p.mem[gm].N;
       void* ym = p.mem[gm].y;
       const int rows = min(BN, p.M - m0);
@@ -990,22 +1037,30 @@ constexpr size_t smem_bytes() {
   return 1024 /*align slack*/ + pair_table_bytes<BN>() + size_t(cst_for<BN>()) * sub_for<BN>() * (128 * kCodeBytes + BN * kRowBytes);
 }
 
-template <int BN, bool BF16, bool MULTI>
+template <int BN, bool BF16, int NM>
 constexpr auto kernel_for() {
-  return nf4_gemm_kernel<BN, groups_for<BN>(), sub_for<BN>(), cst_for<BN>(), nacc_for<BN>(), BF16, MULTI>;
+  return nf4_gemm_kernel<BN, groups_for<BN>(), sub_for<BN>(), cst_for<BN>(), nacc_for<BN>(), BF16, NM>;
 }
 
-template <int BN, bool BF16, bool MULTI>
-static cudaError_t launch1(const GemmParams& p, const CodeMaps& mc, const CUtensorMap& mx, dim3 grid,
+template <int BN, bool BF16, int NM>
+static cudaError_t launch1(const GemmParamsT<kMaxMembers>& pm, const MapsT<kMaxMembers>& mm, dim3 grid,
                            cudaStream_t s) {
-  auto k = kernel_for<BN, BF16, MULTI>();
-  CodeMapsT<MULTI ? kMaxMembers : 1> maps;
-  memcpy(&maps, &mc, sizeof(maps));
+  auto k = kernel_for<BN, BF16, NM>();
+  // the single-weight kernel takes a 1-member parameter block (less to copy per launch)
+  static thread_local GemmParamsT<NM> p;
+  static thread_local MapsT<NM> maps;
+  static_cast<GemmCommon&>(p) = static_cast<const GemmCommon&>(pm);
+  for (int i = 0; i < NM && i < pm.nmem; ++i) {
+    p.mem[i] = pm.mem[i];
+    maps.c[i] = mm.c[i];
+    maps.x[i] = mm.x[i];
+  }
   constexpr size_t sm = smem_bytes<BN>();
-  // 227 KB per block, minus the static shared memory (LUT, code2 tables, barriers: < 6 KB)
+  // 227 KB per block, minus the static shared memory (LUT, barriers: < 2 KB)
   static_assert(sm + 6 * 1024 <= 232448, "shared-memory budget (stages + pair table) exceeded");
-  static_assert(nacc_for<BN>() * (BN < 32 ? 32 : BN) + groups_for<BN>() * sub_for<BN>() * 32 <= 512, "TMEM budget");
+  static_assert(nacc_for<BN>() * (BN < 32 ? 32 : BN) + slots_for<BN>() * sub_for<BN>() * 32 <= 512, "TMEM budget");
   static_assert(cst_for<BN>() >= groups_for<BN>(), "a super-stage slot must not be two phases behind any group");
+  static_assert(sizeof(GemmParamsT<NM>) + sizeof(MapsT<NM>) <= 32000, "kernel parameter space");
   // the dynamic shared-memory opt-in is a per-device (per-context) attribute: set it once
   // per device and instantiation, and never cache a failure
   static std::atomic<uint64_t> attr_set{0};  // bit d: set on device d (d < 64; others set every call)
@@ -1018,7 +1073,7 @@ static cudaError_t launch1(const GemmParams& p, const CodeMaps& mc, const CUtens
     attr_set.fetch_or(bit, std::memory_order_acq_rel);
   }
   // launched with programmatic stream serialization (the kernel executes
-  // griddepcontrol.wait before reading any input)
+  // griddepcontrol.wait before reading anything the previous kernel may write)
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(threads_for<BN>());
@@ -1029,15 +1084,17 @@ static cudaError_t launch1(const GemmParams& p, const CodeMaps& mc, const CUtens
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, k, p, maps, mx);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, k, p, maps);
   if (e != cudaSuccess) return e;
   return cudaPeekAtLastError();
 }
 
 template <int BN, bool BF16>
-static cudaError_t launch(const GemmParams& p, const CodeMaps& mc, const CUtensorMap& mx, dim3 grid,
+static cudaError_t launch(const GemmParamsT<kMaxMembers>& p, const MapsT<kMaxMembers>& m, dim3 grid,
                           cudaStream_t s) {
-  return p.nmem > 1 ? launch1<BN, BF16, true>(p, mc, mx, grid, s) : launch1<BN, BF16, false>(p, mc, mx, grid, s);
+  return p.nmem == 1 ? launch1<BN, BF16, 1>(p, m, grid, s)
+         : p.nmem <= NF4_GEMM_MAX_GROUP ? launch1<BN, BF16, NF4_GEMM_MAX_GROUP>(p, m, grid, s)
+                                        : launch1<BN, BF16, kMaxMembers>(p, m, grid, s);
 }
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -1109,23 +1166,46 @@ static int pick_bn(int M) {
   return 256;
 }
 
-// Stream-K geometry: G resident CTAs (at most one per 4 chunks so every range
-// is non-empty), W chunks in total, and the largest number of segments any
-// tile is split into (= partial slots the workspace needs).
+static std::atomic<int32_t> g_early_weights{1};
+
+// One problem as the host sees it: Y = X . W^T, W an NF4 weight [N, K].
+struct HostMember {
+  const void* x;
+  int32_t K;
+  const uint8_t* packed;
+  const float* absmax;
+  const nf4_dq_state* dq;
+  int32_t N;
+  void* y;
+};
+
+// Stream-K geometry over the member-major chunk stream: G resident CTAs (at most
+// one per 4 chunks so every range is non-empty), W chunks in total, and the
+// largest number of segments any tile is split into (= partial slots the
+// workspace needs).
 struct SkGeom {
-  int bn, tiles_n, tiles_m, nk, align4;
+  int bn, tiles_m, tiles_n, tiles, align4, nk_max;
   int64_t W, G;
   int max_parts;
 };
-static SkGeom sk_geometry(int M, int N, int K) {
+static SkGeom sk_geometry(int M, const int32_t* N, const int32_t* K, int count) {
   SkGeom g;
   g.bn = pick_bn(M);
-  g.tiles_n = (N + 127) / 128;
   g.tiles_m = (M + g.bn - 1) / g.bn;
-  g.nk = K / 64;
-  g.align4 = (g.nk % 4) == 0;
-  g.W = int64_t(g.tiles_n) * g.tiles_m * g.nk;
-  const int64_t cap = sm_count();   // one CTA per SM (the kernel's 3 producer groups fill it)
+  g.tiles_n = 0;
+  g.align4 = 1;
+  g.nk_max = 0;
+  g.W = 0;
+  for (int i = 0; i < count; ++i) {
+    if (N[i] <= 0) continue;
+    const int tn = (N[i] + 127) / 128, nk = K[i] / 64;
+    g.tiles_n += tn;
+    g.W += int64_t(tn) * g.tiles_m * nk;
+    g.align4 = g.align4 && (nk % 4) == 0;
+    g.nk_max = nk > g.nk_max ? nk : g.nk_max;
+  }
+  g.tiles = g.tiles_n * g.tiles_m;
+  const int64_t cap = sm_count();   // one CTA per SM (the kernel's producer groups fill it)
   const int64_t lim = g.align4 ? g.W / 4 : g.W;
   g.G = cap < lim ? cap : lim;
   if (g.G < 1) g.G = 1;
@@ -1133,47 +1213,60 @@ static SkGeom sk_geometry(int M, int N, int K) {
   // every range but the first touching a tile holds >= Lmin of its chunks.
   int64_t lmin = g.W / g.G - (g.align4 ? 4 : 0);
   if (lmin < (g.align4 ? 4 : 1)) lmin = g.align4 ? 4 : 1;
-  int64_t mp = 1 + (g.nk - 1 + lmin - 1) / lmin;
+  int64_t mp = 1 + (g.nk_max - 1 + lmin - 1) / lmin;
   if (mp > g.G) mp = g.G;
   g.max_parts = int(mp);
   return g;
 }
 
-// stream-K workspace: per-tile counters (zero between calls), then the partials
-static int64_t sk_flag_bytes(const SkGeom& g) {
-  return (int64_t(g.tiles_n) * g.tiles_m * 4 + 255) / 256 * 256;
+// Workspace head: one counter per tile (stream-K), 256-B rounded; the fp32
+// partials (stream-K pieces or classic splits) always start after it, so a
+// classic call never writes where a later stream-K call expects zero counters.
+static int64_t flag_bytes(int64_t tiles) { return (tiles * 4 + 255) / 256 * 256; }
+
+// Stream-K workspace, -1 when the chunk stream exceeds the kernel's 32-bit indices
+// (a single weight then takes the classic grid).
+static int64_t streamk_ws_bytes(int M, const int32_t* N, const int32_t* K, int count) {
+  const SkGeom g = sk_geometry(M, N, K, count);
+  if (g.W >= (int64_t(1) << 31)) return -1;
+  return g.max_parts > 1 ? flag_bytes(g.tiles) + int64_t(g.max_parts) * M * g.tiles_n * 128 * 4 : 0;
 }
 
 static int64_t npad_of(int32_t N) { return int64_t((N + 127) / 128) * 128; }
 
-// Stream-K workspace for an [M, K] x [Npad, K]^T problem, -1 when the chunk
-// stream exceeds the kernel's 32-bit indices (the caller then needs the classic grid).
-static int64_t streamk_ws_bytes(int32_t M, int64_t Npad, int32_t K) {
-  const SkGeom g = sk_geometry(M, int32_t(Npad), K);
-  if (g.W >= (int64_t(1) << 31)) return -1;
-  return g.max_parts > 1 ? sk_flag_bytes(g) + int64_t(g.max_parts) * M * Npad * 4 : 0;
+static int64_t classic_ws_bytes(int M, int N, int splits) {
+  if (splits <= 1) return 0;
+  const int64_t tiles = ((N + 127) / 128) * int64_t((M + pick_bn(M) - 1) / pick_bn(M));
+  return flag_bytes(tiles) + int64_t(splits) * M * npad_of(N) * 4;
 }
 
 extern "C" int64_t nf4_gemm_workspace_bytes(int32_t M, int32_t N, int32_t K, int32_t splits) {
   if (M <= 0 || N <= 0 || K <= 0) return 0;
   if (splits <= 0) {
     if (K % 64 != 0) return 0;
-    const int64_t b = streamk_ws_bytes(M, npad_of(N), K);
+    const int64_t b = streamk_ws_bytes(M, &N, &K, 1);
     if (b >= 0) return b;
     splits = nf4_gemm_default_splits(M, N, K);   // classic fallback (nf4_gemm does the same)
   }
-  if (splits <= 1) return 0;
-  return int64_t(splits) * M * npad_of(N) * 4;
+  return classic_ws_bytes(M, N, splits);
 }
 
 extern "C" int64_t nf4_gemm_grouped_workspace_bytes(int32_t M, const int32_t* N, int32_t count, int32_t K) {
-  if (M <= 0 || K <= 0 || K % 64 != 0 || !N || count <= 0 || count > kMaxMembers) return 0;
-  int64_t npad = 0;
+  if (M <= 0 || K <= 0 || K % 64 != 0 || !N || count <= 0 || count > NF4_GEMM_MAX_GROUP) return 0;
+  int32_t Ks[NF4_GEMM_MAX_GROUP];
   for (int i = 0; i < count; ++i) {
     if (N[i] <= 0) return 0;
-    npad += npad_of(N[i]);
+    Ks[i] = K;
   }
-  const int64_t b = streamk_ws_bytes(M, npad, K);
+  const int64_t b = streamk_ws_bytes(M, N, Ks, count);
+  return b > 0 ? b : 0;
+}
+
+extern "C" int64_t nf4_gemm_multi_workspace_bytes(int32_t M, const int32_t* N, const int32_t* K, int32_t count) {
+  if (M <= 0 || !N || !K || count <= 0 || count > NF4_GEMM_MAX_MULTI) return 0;
+  for (int i = 0; i < count; ++i)
+    if (N[i] < 0 || K[i] <= 0 || K[i] % 64 != 0) return 0;
+  const int64_t b = streamk_ws_bytes(M, N, K, count);
   return b > 0 ? b : 0;
 }
 
@@ -1199,123 +1292,126 @@ extern "C" int32_t nf4_gemm_default_splits(int32_t M, int32_t N, int32_t K) {
   return best_s;
 }
 
-// One weight as the host sees it (nf4_gemm: one; nf4_gemm_grouped: up to 4).
-struct HostMember {
-  const uint8_t* packed;
-  const float* absmax;
-  const nf4_dq_state* dq;
-  int32_t N;
-  void* y;
-};
-
-static nf4_status check_member(const HostMember& m, nf4_dtype y_dtype) {
-  if (m.N < 0) return NF4_ERR_BAD_SIZE;
+static nf4_status check_member(const HostMember& m, nf4_dtype y_dtype, int32_t blocksize) {
+  if (m.N < 0 || m.K < 0) return NF4_ERR_BAD_SIZE;
   if ((m.absmax == nullptr) == (m.dq == nullptr)) return NF4_ERR_BAD_STATE;
   if (m.dq && m.dq->blocksize2 != 256) return NF4_ERR_BAD_STATE;
   if (m.N == 0) return NF4_OK;
-  if (!m.packed || !m.y) return NF4_ERR_NULL_POINTER;
+  if (m.K % 64 != 0 || m.K % blocksize != 0) return NF4_ERR_BAD_SIZE;  // a 64-chunk never spans two blocks
+  if (!m.packed || !m.y || !m.x) return NF4_ERR_NULL_POINTER;
   if (m.dq && (!m.dq->qabsmax || !m.dq->code2 || !m.dq->absmax2)) return NF4_ERR_NULL_POINTER;
-  if (!aligned(m.packed, 16)) return NF4_ERR_MISALIGNED;
+  if (!aligned(m.packed, 16) || !aligned(m.x, 16)) return NF4_ERR_MISALIGNED;
   if (!aligned(m.y, y_dtype == NF4_F32 ? 4 : 2)) return NF4_ERR_MISALIGNED;
   if (m.absmax && !aligned(m.absmax, 4)) return NF4_ERR_MISALIGNED;
   return NF4_OK;
 }
 
-static nf4_status gemm_run(const void* x, nf4_dtype x_dtype, int32_t M, int32_t K, int32_t blocksize,
-                           const HostMember* mem_in, int32_t count, nf4_dtype y_dtype, int32_t splits, void* workspace,
+static nf4_status gemm_run(nf4_dtype x_dtype, int32_t M, int32_t blocksize, const HostMember* mem_in,
+                           int32_t count, nf4_dtype y_dtype, int32_t splits, void* workspace,
                            int64_t workspace_bytes, void* stream) {
-  if (M < 0 || K < 0 || count < 1 || count > kMaxMembers) return NF4_ERR_BAD_SIZE;
+  if (M < 0 || count < 1 || count > kMaxMembers) return NF4_ERR_BAD_SIZE;
   if (x_dtype != NF4_F16 && x_dtype != NF4_BF16) return NF4_ERR_BAD_DTYPE;
   if (y_dtype != NF4_F16 && y_dtype != NF4_BF16 && y_dtype != NF4_F32) return NF4_ERR_BAD_DTYPE;
   if (!is_pow2(blocksize) || blocksize < 64 || blocksize > 4096) return NF4_ERR_BAD_BLOCKSIZE;
   for (int i = 0; i < count; ++i) {
-    const nf4_status st = check_member(mem_in[i], y_dtype);
+    if (mem_in[i].K < 0 || mem_in[i].N < 0) return NF4_ERR_BAD_SIZE;
+    if (M == 0 || mem_in[i].N == 0 || mem_in[i].K == 0) {
+      // nothing to compute, but the state must still be consistent
+      if ((mem_in[i].absmax == nullptr) == (mem_in[i].dq == nullptr)) return NF4_ERR_BAD_STATE;
+      if (mem_in[i].dq && mem_in[i].dq->blocksize2 != 256) return NF4_ERR_BAD_STATE;
+      if (mem_in[i].K % 64 != 0 || mem_in[i].K % blocksize != 0) return NF4_ERR_BAD_SIZE;
+      continue;
+    }
+    const nf4_status st = check_member(mem_in[i], y_dtype, blocksize);
     if (st != NF4_OK) return st;
   }
-  // members with N == 0 contribute no tiles
+  // problems with N == 0 or K == 0 contribute no tiles (K == 0 with N > 0: Y = 0)
   HostMember mem[kMaxMembers];
   int nmem = 0;
-  for (int i = 0; i < count; ++i)
-    if (mem_in[i].N > 0) mem[nmem++] = mem_in[i];
-  if (M == 0 || nmem == 0) { set_launch_count(0); return NF4_OK; }
-  if (K % 64 != 0 || K % blocksize != 0) return NF4_ERR_BAD_SIZE;  // a 64-chunk never spans two blocks
-  if (!x) return NF4_ERR_NULL_POINTER;
-  if (!aligned(x, 16)) return NF4_ERR_MISALIGNED;
-  const int nk = K / 64;
+  for (int i = 0; i < count; ++i) {
+    if (M == 0 || mem_in[i].N == 0) continue;
+    if (mem_in[i].K == 0) {
+      const size_t bytes = size_t(M) * mem_in[i].N * (y_dtype == NF4_F32 ? 4 : 2);
+      if (cudaMemsetAsync(mem_in[i].y, 0, bytes, static_cast<cudaStream_t>(stream)) != cudaSuccess)
+        return NF4_ERR_CUDA;
+      continue;
+    }
+    mem[nmem++] = mem_in[i];
+  }
+  if (nmem == 0) { set_launch_count(0); return NF4_OK; }
   const int bn = pick_bn(M);
-  int tiles_n = 0;
-  for (int i = 0; i < nmem; ++i) tiles_n += (mem[i].N + 127) / 128;
-  const int64_t npad = int64_t(tiles_n) * 128;
+  int32_t Ns[kMaxMembers], Ks[kMaxMembers];
+  for (int i = 0; i < nmem; ++i) { Ns[i] = mem[i].N; Ks[i] = mem[i].K; }
+  const SkGeom g = sk_geometry(M, Ns, Ks, nmem);
+  const int64_t npad = int64_t(g.tiles_n) * 128;
   // stream-K chunk indices are 32-bit in the kernel; beyond that, the classic grid (one weight only)
-  const int64_t w_chunks = int64_t(tiles_n) * ((M + bn - 1) / bn) * nk;
-  const bool streamk = (splits <= 0 || nmem > 1) && nk > 0 && w_chunks < (int64_t(1) << 31);
+  const bool streamk = (splits <= 0 || nmem > 1) && g.W < (int64_t(1) << 31);
   if (!streamk && nmem > 1) return NF4_ERR_BAD_SIZE;
-  if (splits <= 0 && !streamk) splits = nf4_gemm_default_splits(M, mem[0].N, K);
-  SkGeom g{};
+  const int nk0 = mem[0].K / 64;
+  if (splits <= 0 && !streamk) splits = nf4_gemm_default_splits(M, mem[0].N, mem[0].K);
   if (streamk) {
-    g = sk_geometry(M, int32_t(npad), K);
     if (g.max_parts > 1) {
       if (!workspace) return NF4_ERR_NULL_POINTER;
-      if (workspace_bytes < sk_flag_bytes(g) + int64_t(g.max_parts) * M * npad * 4) return NF4_ERR_BAD_STATE;
+      if (workspace_bytes < flag_bytes(g.tiles) + int64_t(g.max_parts) * M * npad * 4) return NF4_ERR_BAD_STATE;
       if (!aligned(workspace, 16)) return NF4_ERR_MISALIGNED;
     }
     splits = 1;
   } else {
     if (splits <= 0) splits = 1;
-    if (splits > nk) splits = nk > 0 ? nk : 1;
-    if (splits > 1) {
-      if (!workspace) return NF4_ERR_NULL_POINTER;
-      if (workspace_bytes < int64_t(splits) * M * npad * 4) return NF4_ERR_BAD_STATE;
-      if (!aligned(workspace, 16)) return NF4_ERR_MISALIGNED;
-    }
+    if (splits > nk0) splits = nk0 > 0 ? nk0 : 1;
   }
-  GemmParams p;
-  int tile0 = 0;
-  for (int i = 0; i < kMaxMembers; ++i) {
+  static thread_local GemmParamsT<kMaxMembers> p;
+  int tile0 = 0, ftile0 = 0, cbase = 0;
+  for (int i = 0; i < nmem; ++i) {
     Member& m = p.mem[i];
-    if (i < nmem) {
-      m.absmax = mem[i].absmax;
-      m.qabsmax = mem[i].dq ? mem[i].dq->qabsmax : nullptr;
-      m.code2 = mem[i].dq ? mem[i].dq->code2 : nullptr;
-      m.absmax2 = mem[i].dq ? mem[i].dq->absmax2 : nullptr;
-      m.offset = mem[i].dq ? mem[i].dq->offset : 0.0f;
-      m.N = mem[i].N;
-      m.y = mem[i].y;
-      m.tile0 = tile0;
-      tile0 += (mem[i].N + 127) / 128;
-    } else {
-      m = Member{};
-      m.tile0 = 1 << 30;
-    }
+    m.absmax = mem[i].absmax;
+    m.qabsmax = mem[i].dq ? mem[i].dq->qabsmax : nullptr;
+    m.code2 = mem[i].dq ? mem[i].dq->code2 : nullptr;
+    m.absmax2 = mem[i].dq ? mem[i].dq->absmax2 : nullptr;
+    m.offset = mem[i].dq ? mem[i].dq->offset : 0.0f;
+    m.N = mem[i].N;
+    m.y = mem[i].y;
+    m.K = mem[i].K;
+    m.nk = mem[i].K / 64;
+    m.tiles_n = (mem[i].N + 127) / 128;
+    m.tile0 = tile0;
+    m.ftile0 = ftile0;
+    m.cbase = cbase;
+    tile0 += m.tiles_n;
+    ftile0 += m.tiles_n * g.tiles_m;
+    cbase += m.tiles_n * g.tiles_m * m.nk;
   }
   p.nmem = nmem;
-  p.x = static_cast<const uint16_t*>(x);
   p.partial = static_cast<float*>(workspace);
   p.flags = nullptr;
   if (streamk && g.max_parts > 1) {
     p.flags = static_cast<unsigned*>(workspace);
-    p.partial = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + sk_flag_bytes(g));
+    p.partial = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + flag_bytes(g.tiles));
   }
   p.M = M;
-  p.K = K;
   p.Npad = int32_t(npad);
   p.bs_shift = log2i(blocksize);
   const int sub = sub_of(bn);
   {
     // whole super-stages per split (SUB chunks share one TMA box); splits = non-empty ranges
-    int cps = (nk + splits - 1) / splits;
+    int cps = (nk0 + splits - 1) / splits;
     cps = (cps + sub - 1) / sub * sub;
-    splits = (nk + cps - 1) / cps;
+    splits = (nk0 + cps - 1) / cps;
     p.chunks_per_split = cps;
   }
   p.splits = splits;
+  if (!streamk && splits > 1) {
+    if (!workspace) return NF4_ERR_NULL_POINTER;
+    if (workspace_bytes < classic_ws_bytes(M, mem[0].N, splits)) return NF4_ERR_BAD_STATE;
+    if (!aligned(workspace, 16)) return NF4_ERR_MISALIGNED;
+    p.partial = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + flag_bytes(g.tiles));
+  }
   p.out_dtype = int(y_dtype);
   p.streamk = streamk ? 1 : 0;
-  p.tiles_n = tiles_n;
-  p.tiles_m = (M + bn - 1) / bn;
-  p.nk = nk;
-  p.total_chunks = int64_t(p.tiles_n) * p.tiles_m * nk;
+  p.tiles_m = g.tiles_m;
+  p.total_chunks = g.W;
   p.align4 = streamk ? g.align4 : 0;
+  p.early_weights = g_early_weights.load(std::memory_order_relaxed);
   p.trace = nullptr;
   p.experiment = 0;
 #if NF4_GEMM_DIAG
@@ -1323,28 +1419,31 @@ static nf4_status gemm_run(const void* x, nf4_dtype x_dtype, int32_t M, int32_t 
   if (const char* ex = getenv("NF4_GEMM_EXPERIMENT")) p.experiment = atoi(ex);
 #endif
   nf4_codebook(p.lut);
-  dim3 grid = streamk ? dim3(unsigned(g.G), 1, 1) : dim3(unsigned(tiles_n), unsigned(p.tiles_m), unsigned(splits));
+  dim3 grid = streamk ? dim3(unsigned(g.G), 1, 1) : dim3(unsigned(g.tiles_n), unsigned(g.tiles_m), unsigned(splits));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool bf16 = x_dtype == NF4_BF16;
-  CodeMaps mc;
-  memset(&mc, 0, sizeof(mc));
-  CUtensorMap mx;
+  static thread_local MapsT<kMaxMembers> maps;
   const CUtensorMapSwizzle csw = sub == 4 ? CU_TENSOR_MAP_SWIZZLE_128B
                                  : sub == 2 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
-  for (int i = 0; i < nmem; ++i)
-    if (!make_map(&mc.m[i], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, mem[i].packed, uint64_t(K) / 2, uint64_t(mem[i].N),
-                  uint32_t(sub * kCodeBytes), 128, csw))
+  for (int i = 0; i < nmem; ++i) {
+    if (!make_map(&maps.c[i], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, mem[i].packed, uint64_t(mem[i].K) / 2,
+                  uint64_t(mem[i].N), uint32_t(sub * kCodeBytes), 128, csw))
       return NF4_ERR_CUDA;
-  if (!make_map(&mx, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, x, uint64_t(K),
-                uint64_t(M), kChunk, uint32_t(bn), CU_TENSOR_MAP_SWIZZLE_128B))
-    return NF4_ERR_CUDA;
+    if (i > 0 && mem[i].x == mem[i - 1].x && mem[i].K == mem[i - 1].K) {
+      maps.x[i] = maps.x[i - 1];
+    } else if (!make_map(&maps.x[i], bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
+                         mem[i].x, uint64_t(mem[i].K), uint64_t(M), kChunk, uint32_t(bn),
+                         CU_TENSOR_MAP_SWIZZLE_128B)) {
+      return NF4_ERR_CUDA;
+    }
+  }
   cudaError_t e;
   switch (bn) {
-    case 16: e = bf16 ? launch<16, true>(p, mc, mx, grid, s) : launch<16, false>(p, mc, mx, grid, s); break;
-    case 32: e = bf16 ? launch<32, true>(p, mc, mx, grid, s) : launch<32, false>(p, mc, mx, grid, s); break;
-    case 64: e = bf16 ? launch<64, true>(p, mc, mx, grid, s) : launch<64, false>(p, mc, mx, grid, s); break;
-    case 128: e = bf16 ? launch<128, true>(p, mc, mx, grid, s) : launch<128, false>(p, mc, mx, grid, s); break;
-    default: e = bf16 ? launch<256, true>(p, mc, mx, grid, s) : launch<256, false>(p, mc, mx, grid, s); break;
+    case 16: e = bf16 ? launch<16, true>(p, maps, grid, s) : launch<16, false>(p, maps, grid, s); break;
+    case 32: e = bf16 ? launch<32, true>(p, maps, grid, s) : launch<32, false>(p, maps, grid, s); break;
+    case 64: e = bf16 ? launch<64, true>(p, maps, grid, s) : launch<64, false>(p, maps, grid, s); break;
+    case 128: e = bf16 ? launch<128, true>(p, maps, grid, s) : launch<128, false>(p, maps, grid, s); break;
+    default: e = bf16 ? launch<256, true>(p, maps, grid, s) : launch<256, false>(p, maps, grid, s); break;
   }
   if (e != cudaSuccess) { cudaGetLastError(); return NF4_ERR_CUDA; }
   int launches = 1;
@@ -1352,8 +1451,8 @@ static nf4_status gemm_run(const void* x, nf4_dtype x_dtype, int32_t M, int32_t 
     const int64_t mn = int64_t(M) * mem[0].N;
     int64_t gr = (mn + 255) / 256;
     if (gr > int64_t(sm_count()) * 8) gr = int64_t(sm_count()) * 8;
-    nf4_gemm_reduce_kernel<<<int(gr), 256, 0, s>>>(static_cast<const float*>(workspace), splits, M, mem[0].N,
-                                                   int(npad), mem[0].y, int(y_dtype));
+    nf4_gemm_reduce_kernel<<<int(gr), 256, 0, s>>>(p.partial, splits, M, mem[0].N, int(npad), mem[0].y,
+                                                   int(y_dtype));
     if (cudaPeekAtLastError() != cudaSuccess) { cudaGetLastError(); return NF4_ERR_CUDA; }
     ++launches;
   }
@@ -1365,9 +1464,9 @@ extern "C" nf4_status nf4_gemm(const void* x, nf4_dtype x_dtype, int32_t M, cons
                                const float* absmax, const nf4_dq_state* dq, int32_t N, int32_t K, int32_t blocksize,
                                void* y, nf4_dtype y_dtype, int32_t splits, void* workspace,
                                int64_t workspace_bytes, void* stream) {
-  if (N < 0) return NF4_ERR_BAD_SIZE;
-  const HostMember m{packed, absmax, dq, N, y};
-  return gemm_run(x, x_dtype, M, K, blocksize, &m, 1, y_dtype, splits, workspace, workspace_bytes, stream);
+  if (N < 0 || K < 0) return NF4_ERR_BAD_SIZE;
+  const HostMember m{x, K, packed, absmax, dq, N, y};
+  return gemm_run(x_dtype, M, blocksize, &m, 1, y_dtype, splits, workspace, workspace_bytes, stream);
 }
 
 extern "C" nf4_status nf4_gemm_grouped(const void* x, nf4_dtype x_dtype, int32_t M, int32_t K, int32_t blocksize,
@@ -1375,10 +1474,28 @@ extern "C" nf4_status nf4_gemm_grouped(const void* x, nf4_dtype x_dtype, int32_t
                                        void* workspace, int64_t workspace_bytes, void* stream) {
   if (count < 1 || count > NF4_GEMM_MAX_GROUP) return NF4_ERR_BAD_SIZE;
   if (!weights) return NF4_ERR_NULL_POINTER;
-  HostMember m[kMaxMembers];
+  if (K < 0) return NF4_ERR_BAD_SIZE;
+  HostMember m[NF4_GEMM_MAX_GROUP];
   for (int i = 0; i < count; ++i) {
     const nf4_gemm_weight& w = weights[i];
-    m[i] = HostMember{w.packed, w.absmax, w.absmax ? nullptr : &w.dq, w.N, w.y};
+    m[i] = HostMember{x, K, w.packed, w.absmax, w.absmax ? nullptr : &w.dq, w.N, w.y};
   }
-  return gemm_run(x, x_dtype, M, K, blocksize, m, count, y_dtype, 0, workspace, workspace_bytes, stream);
+  return gemm_run(x_dtype, M, blocksize, m, count, y_dtype, 0, workspace, workspace_bytes, stream);
+}
+
+extern "C" nf4_status nf4_gemm_multi(const nf4_gemm_problem* problems, int32_t count, int32_t M, nf4_dtype x_dtype,
+                                     int32_t blocksize, nf4_dtype y_dtype, void* workspace, int64_t workspace_bytes,
+                                     void* stream) {
+  if (count < 1 || count > NF4_GEMM_MAX_MULTI) return NF4_ERR_BAD_SIZE;
+  if (!problems) return NF4_ERR_NULL_POINTER;
+  HostMember m[NF4_GEMM_MAX_MULTI];
+  for (int i = 0; i < count; ++i) {
+    const nf4_gemm_problem& q = problems[i];
+    m[i] = HostMember{q.x, q.K, q.packed, q.absmax, q.absmax ? nullptr : &q.dq, q.N, q.y};
+  }
+  return gemm_run(x_dtype, M, blocksize, m, count, y_dtype, 0, workspace, workspace_bytes, stream);
+}
+
+extern "C" void nf4_gemm_set_early_weight_reads(int32_t enable) {
+  g_early_weights.store(enable ? 1 : 0, std::memory_order_relaxed);
 }

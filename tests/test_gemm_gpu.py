@@ -425,3 +425,128 @@ def test_gemm_grouped_sparse_pm1_exact_and_full_weights(nf4, orc, M):
         want = orc.dequantize(packs[i], N * K, 64, orc.OUT_BF16, threads=8, **kws[i]).view(
             ml_dtypes.bfloat16).astype(np.float32).reshape(N, K)
         assert np.array_equal(_pos0(w_gpu[i]), _pos0(want)), (M, i)
+
+
+# ---------------------------------------------------------------------------
+# nf4_gemm_multi: independent problems (own X and K) in one persistent launch
+# ---------------------------------------------------------------------------
+MULTI_SHAPES = [(512, 1024, True), (200, 2048, False), (384, 512, True), (128, 3072, False), (640, 256, True),
+                (256, 1536, True), (130, 768, False)]
+
+
+def _multi_setup(nf4, M, xdt, seed0, shapes=MULTI_SHAPES, sparse=True):
+    import torch
+    probs, host = [], []
+    for i, (N, K, dq) in enumerate(shapes):
+        packed, kw = _weights(N, K, 64, dq, seed=seed0 + i)
+        x16 = _to16(_sparse_pm1(M, K, 64, seed0 + 7 * i) if sparse else
+                    np.random.Generator(np.random.Philox(seed0 + i)).standard_normal((M, K)).astype(np.float32), xdt)
+        x = _x_tensor(x16, xdt, M, K)
+        if dq:
+            probs.append((x, K, dev(packed), None,
+                          nf4.DQ(dev(kw["qabsmax"]), dev(kw["code2"]), dev(kw["absmax2"]), kw["offset"]), N))
+        else:
+            probs.append((x, K, dev(packed), dev(kw["absmax"]), None, N))
+        host.append((x16, packed, kw, N, K))
+    return probs, host
+
+
+@pytest.mark.parametrize("M", [1, 16, 40, 100])
+@pytest.mark.parametrize("xdt", ["bf16", "f16"])
+def test_gemm_multi_exact_sums(nf4, orc, M, xdt):
+    """Seven problems with different N, K, scale formats and their own X in one
+    launch: every Y_i equals the exact fp64 oracle product (sparse +-1 X)."""
+    import torch
+    probs, host = _multi_setup(nf4, M, xdt, 900 + M)
+    ys = nf4.nf4_gemm_multi(probs, M=M, x_dtype=xdt, y_dtype="f32")
+    torch.cuda.synchronize()
+    assert nf4.nf4_last_launch_count() == 1
+    for i, (x16, packed, kw, N, K) in enumerate(host):
+        ref = _exact_reference(x16, xdt, packed, N, K, 64, kw, orc)
+        assert np.array_equal(_pos0(ys[i].cpu().numpy()), _pos0(ref.astype(np.float32))), (M, i)
+
+
+@pytest.mark.parametrize("M", [1, 16, 64])
+def test_gemm_multi_recovers_every_weight(nf4, orc, M):
+    """Identity blocks over each problem's own K recover every weight of every
+    problem bit-exactly through one launch per block."""
+    import torch
+    shapes = [(256, 512, True), (136, 1024, False), (384, 256, True)]
+    kmax = max(K for _, K, _ in shapes)
+    probs0, host = _multi_setup(nf4, M, "bf16", 40 + M, shapes)
+    w_gpu = [np.zeros((N, K), np.float32) for N, K, _ in shapes]
+    ws = torch.zeros(max(16, nf4.nf4_gemm_multi_workspace_bytes(M, [s[0] for s in shapes], [s[1] for s in shapes])),
+                     dtype=torch.uint8, device="cuda")
+    for k0 in range(0, kmax, M):
+        probs = []
+        for (x, K, pk, a, d, N) in probs0:
+            xe = np.zeros((M, K), np.float32)
+            m_eff = max(0, min(M, K - k0))
+            xe[np.arange(m_eff), k0 + np.arange(m_eff)] = 1.0
+            probs.append((_x_tensor(_to16(xe, "bf16"), "bf16", M, K), K, pk, a, d, N))
+        ys = nf4.nf4_gemm_multi(probs, M=M, x_dtype="bf16", y_dtype="f32", workspace=ws)
+        torch.cuda.synchronize()
+        for i, (N, K, _) in enumerate(shapes):
+            m_eff = max(0, min(M, K - k0))
+            if m_eff:
+                w_gpu[i][:, k0:k0 + m_eff] = ys[i].cpu().numpy()[:m_eff].T
+    for i, (x16, packed, kw, N, K) in enumerate(host):
+        want = orc.dequantize(packed, N * K, 64, orc.OUT_BF16, threads=8, **kw).view(
+            ml_dtypes.bfloat16).astype(np.float32).reshape(N, K)
+        assert np.array_equal(_pos0(w_gpu[i]), _pos0(want)), (M, i)
+
+
+def test_gemm_multi_random_bound_workspace_reuse_and_late_weights(nf4, orc):
+    """Random X within the fp32 bound; one workspace reused across calls; the
+    late-weight-read mode (every read after griddepcontrol.wait) gives the same
+    bits; classic split-K on the same workspace does not disturb later stream-K."""
+    import torch
+    M = 24
+    probs, host = _multi_setup(nf4, M, "bf16", 77, sparse=False)
+    ws = torch.zeros(nf4.nf4_gemm_multi_workspace_bytes(M, [h[3] for h in host], [h[4] for h in host]),
+                     dtype=torch.uint8, device="cuda")
+    a = [y.clone() for y in nf4.nf4_gemm_multi(probs, M=M, y_dtype="f32", workspace=ws)]
+    # a classic split-K call writing its partials into the same buffer
+    x, K, pk, am, d, N = probs[1]
+    need = nf4.nf4_gemm_workspace_bytes(M, N, K, 4)
+    big = torch.zeros(max(need, ws.numel()), dtype=torch.uint8, device="cuda")
+    nf4.nf4_gemm(x, pk, am, d, N=N, K=K, y_dtype="f32", splits=4, workspace=big)
+    b = [y.clone() for y in nf4.nf4_gemm_multi(probs, M=M, y_dtype="f32", workspace=big[:ws.numel()])]
+    nf4.nf4_gemm_set_early_weight_reads(False)
+    try:
+        c = nf4.nf4_gemm_multi(probs, M=M, y_dtype="f32", workspace=ws)
+    finally:
+        nf4.nf4_gemm_set_early_weight_reads(True)
+    torch.cuda.synchronize()
+    for i, (x16, packed, kw, N, K) in enumerate(host):
+        assert torch.equal(a[i].view(torch.int32), b[i].view(torch.int32)), i
+        assert torch.equal(a[i].view(torch.int32), c[i].view(torch.int32)), i
+        ref, mag = orc.gemm_reference(x16, orc.OUT_BF16, packed, N, K, 64, **kw)
+        err = np.abs(a[i].cpu().numpy().astype(np.float64) - ref)
+        assert (err <= K * 2.0 ** -23 * mag + 1e-30).all(), i
+    assert int(ws.view(torch.int32)[:64].abs().sum()) == 0
+
+
+def test_gemm_multi_many_problems_and_errors(nf4, orc):
+    """56 problems (the size of an 8-layer step) in one launch, spot-checked; K=0
+    gives Y=0; bad K and too many problems are rejected."""
+    import torch
+    M, K = 16, 512
+    shapes = [(128 + 64 * (i % 3), K * (1 + i % 2), bool(i % 2)) for i in range(56)]
+    probs, host = _multi_setup(nf4, M, "bf16", 5000, shapes)
+    ys = nf4.nf4_gemm_multi(probs, M=M, y_dtype="f32")
+    torch.cuda.synchronize()
+    for i in (0, 1, 27, 55):
+        x16, packed, kw, N, Ki = host[i]
+        ref = _exact_reference(x16, "bf16", packed, N, Ki, 64, kw, orc)
+        assert np.array_equal(_pos0(ys[i].cpu().numpy()), _pos0(ref.astype(np.float32))), i
+    x, _, pk, a, d, N = probs[0]
+    y0 = nf4.nf4_gemm_multi([(x, 0, pk, a, d, N)], M=M, y_dtype="f32")
+    torch.cuda.synchronize()
+    assert int(y0[0].abs().sum()) == 0
+    with pytest.raises(nf4.NF4Error) as e:
+        nf4.nf4_gemm_multi([(x, 96, pk, a, d, N)], M=M)
+    assert e.value.status == 2
+    with pytest.raises(nf4.NF4Error) as e:
+        nf4.nf4_gemm_multi(probs + probs[:9], M=M)
+    assert e.value.status == 2

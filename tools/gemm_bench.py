@@ -42,6 +42,8 @@ def main():
     ap.add_argument("--graph", action="store_true", help="replay each step from a CUDA graph")
     ap.add_argument("--grouped", action="store_true",
                     help="q/k/v and gate/up of each layer as one nf4_gemm_grouped launch (they share X)")
+    ap.add_argument("--multi", action="store_true",
+                    help="all weights of the step as independent problems, nf4_gemm_multi (<= 64 per launch)")
     args = ap.parse_args()
 
     torch.cuda.set_device(0)
@@ -121,7 +123,17 @@ def main():
                 members = [(ws._ptr(ws.codes, ws.entries[i].codes_off), None, dqs[i], tensors[i].rows) for i in grp]
                 nf4.nf4_gemm_grouped(xs[K], members, K=K, ys=[ys[i] for i in grp], workspace=gws[tuple(grp)])
 
-    step = grouped_step if args.grouped else fused_step
+    mws = torch.zeros(max(16, max(nf4.nf4_gemm_multi_workspace_bytes(M, [t.rows for t in tensors[i:i + 64]],
+                                                                      [t.cols for t in tensors[i:i + 64]])
+                                  for i in range(0, len(tensors), 64))), dtype=torch.uint8, device="cuda")
+    probs = [(xs[t.cols], t.cols, ws._ptr(ws.codes, e.codes_off), None, dqs[i], t.rows)
+             for i, (t, e) in enumerate(zip(tensors, ws.entries))]
+
+    def multi_step():
+        for i in range(0, len(probs), 64):
+            nf4.nf4_gemm_multi(probs[i:i + 64], M=M, ys=ys[i:i + 64], workspace=mws)
+
+    step = multi_step if args.multi else grouped_step if args.grouped else fused_step
     if args.graph:
         # the whole step as one CUDA graph (no host launch overhead; PDL edges kept)
         gs = torch.cuda.Stream()
@@ -148,7 +160,8 @@ def main():
            "fused_tweights_per_s": round(n_total / (fused_ms * 1e-3) / 1e12, 3),
            "frac_of_lut_bound": round(n_total / (fused_ms * 1e-3) / 6.48e12, 3),
            "splits": sorted(set(splits.values())), "grouped": bool(args.grouped),
-           "launches_per_step": len(groups) if args.grouped else len(tensors)}
+           "multi": bool(args.multi),
+           "launches_per_step": -(-len(tensors) // 64) if args.multi else len(groups) if args.grouped else len(tensors)}
     if not args.no_unfused:
         wbuf = torch.empty(max(t.n for t in tensors), dtype=torch.bfloat16, device="cuda")
 
