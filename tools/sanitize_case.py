@@ -92,6 +92,31 @@ def main():
         y1 = nf4.nf4_gemm(xg, wp3, wa3, None, N=256, K=256, y_dtype="f32")
         torch.cuda.synchronize()
         bad += int(not (torch.equal(yg[0], y0) and torch.equal(yg[1], y1)))
+    # multi-problem GEMM (own X and K per problem, mixed scale formats, tiles cut into
+    # pieces), launched twice back to back on one workspace; checked vs the oracle bound
+    shapes = [(384, 512, True), (200, 1024, False), (256, 256, True)]
+    probs, refs = [], []
+    for i, (Nm, Km, dqm) in enumerate(shapes):
+        pk = syn.hash_packed(20 + i, 0, Nm * Km // 2)
+        nbm = Nm * Km // 64
+        if dqm:
+            kwm = dict(qabsmax=syn.hash_qabsmax(20 + i, 0, nbm), code2=code2,
+                       absmax2=syn.hash_absmax2(20 + i, 0, -(-nbm // 256)), offset=float(syn.hash_offset(20 + i)))
+        else:
+            kwm = dict(absmax=syn.hash_absmax(20 + i, 0, nbm))
+        xm = syn.gaussian_weights(24 * Km, 30 + i).reshape(24, Km).astype(ml_dtypes.bfloat16).view(np.uint16)
+        xmt = d(xm.view(np.int16)).view(torch.bfloat16)
+        dqm_t = nf4.DQ(d(kwm["qabsmax"]), d(code2), d(kwm["absmax2"]), kwm["offset"]) if dqm else None
+        probs.append((xmt, Km, d(pk), None if dqm else d(kwm["absmax"]), dqm_t, Nm))
+        refs.append(oracle.gemm_reference(xm, oracle.OUT_BF16, pk, Nm, Km, 64, **kwm))
+    wsm = torch.zeros(max(16, nf4.nf4_gemm_multi_workspace_bytes(24, [s_[0] for s_ in shapes],
+                                                                 [s_[1] for s_ in shapes])),
+                      dtype=torch.uint8, device="cuda")
+    for _ in range(2):
+        ym = nf4.nf4_gemm_multi(probs, M=24, y_dtype="f32", workspace=wsm)
+    torch.cuda.synchronize()
+    for (Nm, Km, _), yi, (rf, mg) in zip(shapes, ym, refs):
+        bad += int(not (np.abs(yi.cpu().numpy().astype(np.float64) - rf) <= Km * 2.0 ** -23 * mg + 1e-30).all())
     # synth + sol
     buf8 = torch.empty(8192 * 4, dtype=torch.uint8, device="cuda")
     nf4.nf4_synth_fill(_lib.NF4_SYNTH_CODES, 1, 3, 1000, buf8)
