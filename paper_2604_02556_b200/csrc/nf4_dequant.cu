@@ -72,6 +72,11 @@ static const Variant kVariants[] = {
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 constexpr int kDefaultVariant = 8;   // v2u4sxc: best measured on B200 (profiles/r01_variants.md)
+// Launches of fewer than kQuarterTileWaves x SMs default-size tiles take 4096-element tiles.
+#ifndef NF4_QUARTER_TILE_WAVES
+#define NF4_QUARTER_TILE_WAVES 4
+#endif
+constexpr int kQuarterTileWaves = NF4_QUARTER_TILE_WAVES;
 constexpr int kMaxTileBlocks = 256;  // TILE / 64 for the 16384-element tiles using sscale
 
 struct TensorDesc {
@@ -476,7 +481,7 @@ static void launch_pdl(Kernel k, int grid, cudaStream_t stream, const Params& P,
 }
 
 template <int MAXB>
-static void launch_small(const BatchParams& P, int out, int grid, cudaStream_t stream) {
+static void launch_small(const BatchParams& P, int out, int grid, cudaStream_t stream, bool quarter_tiles) {
   BatchParamsT<MAXB> Q;
   Q.total_tiles = P.total_tiles;
   Q.count = P.count;
@@ -485,7 +490,16 @@ static void launch_small(const BatchParams& P, int out, int grid, cudaStream_t s
   for (int i = 0; i < P.count; ++i) Q.t[i] = P.t[i];
   // about two resident waves of tiles or fewer: latency-bound, issue code loads first
   const bool early = P.total_tiles <= int64_t(2) * sm_count() * 8;
-  if (early) {
+  if (quarter_tiles) {
+    // a few waves' worth of 16384-element tiles would leave SMs idle: 4096-element
+    // tiles (one group per thread) spread the launch over 4x more CTAs
+    if (out == 0)
+      launch_pdl(dequant_kernel<0, 8, 1, false, true, true, true, false, MAXB, true>, grid, stream, Q);
+    else if (out == 1)
+      launch_pdl(dequant_kernel<1, 8, 1, false, true, true, true, false, MAXB, true>, grid, stream, Q);
+    else
+      launch_pdl(dequant_kernel<2, 8, 1, false, true, true, true, false, MAXB, true>, grid, stream, Q);
+  } else if (early) {
     if (out == 0)
       launch_pdl(dequant_kernel<0, 8, 4, false, true, true, true, false, MAXB, true>, grid, stream, Q);
     else if (out == 1)
@@ -552,7 +566,15 @@ static nf4_status validate(const nf4_tensor& t, int out) {
 static nf4_status launch_batch(const nf4_tensor* ts, int count, int out, const float* lut, cudaStream_t stream,
                                int32_t* launches) {
   const int v = out == 2 ? kDefaultVariant : current_variant();
-  const int64_t tile = tile_elems(v);
+  int64_t tile = tile_elems(v);
+  // small launches of the default kernel use quarter-size tiles (more CTAs, all SMs busy)
+  bool quarter = false;
+  if (v == kDefaultVariant && count <= 16) {
+    int64_t t16 = 0;
+    for (int i = 0; i < count; ++i) t16 += (ts[i].n + tile - 1) / tile;
+    quarter = t16 < int64_t(kQuarterTileWaves) * sm_count();
+    if (quarter) tile /= 4;
+  }
   BatchParams P;
   P.count = 0;
   P.pad_ = 0;
@@ -581,8 +603,8 @@ static nf4_status launch_batch(const nf4_tensor* ts, int count, int out, const f
   const int grid = grid_for(v, tiles, out);
   if (v == kDefaultVariant && P.count <= 16) {
     // light parameter block for single tensors and decoder-layer batches
-    if (P.count == 1) launch_small<1>(P, out, grid, stream);
-    else launch_small<16>(P, out, grid, stream);
+    if (P.count == 1) launch_small<1>(P, out, grid, stream, quarter);
+    else launch_small<16>(P, out, grid, stream, quarter);
   } else {
     KernelFn fn = kernel_of(out, v);
     launch_pdl(fn, grid, stream, P, v == 12 ? size_t(kPairBytes) : 0);

@@ -2,10 +2,13 @@
 """BASELINE config 5 sweep: blocksize 64/128/256/4096 x fp16/bf16 x n = 2^20..2^30
 (fp32 absmax primary; --dq for double-quant), 1 GPU, single-tensor nf4_dequantize.
 
-Each point: W warm-up launches, then K timed launches with CUDA events; inputs
-smaller than ~4x L2 are timed with an L2 flush (a 256 MB write) between launches
-and reported as "cold"; larger ones need no flush.  Prints a markdown table and
-writes JSON lines to --out.
+Default method "graph": every point is K launches replayed from one CUDA graph
+(back to back, as a stream of weight dequantizations runs), time per launch =
+graph time / K.  Points whose footprint fits in ~4x L2 rotate over R disjoint
+copies of inputs and outputs (R x footprint > 4 x L2), so every launch is
+L2-cold.  Method "events" (round 1): CUDA events around single launches with a
+512 MB read flush before each cold one -- it carries a ~6 us event/launch floor.
+Prints a markdown table and writes JSON lines to --out.
 """
 from __future__ import annotations
 
@@ -31,6 +34,8 @@ def main():
     ap.add_argument("--max-log2", type=int, default=30)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--method", default="graph", choices=["graph", "events"])
+    ap.add_argument("--launches", type=int, default=64, help="graph method: launches per replay")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     nf4.load()
@@ -56,7 +61,7 @@ def main():
             nf4.nf4_synth_fill(_lib.NF4_SYNTH_ABSMAX2, 6, 0, a2.numel(), a2)
             from synth import inputs as syn
             code2 = torch.from_numpy(syn.dynamic_map_code2()).cuda()
-            dq = nf4.DQ(q, code2, a2, 0.05)
+            dq = True
             absmax = None
         else:
             absmax = torch.empty(nb, dtype=torch.float32, device="cuda")
@@ -66,25 +71,59 @@ def main():
             for lg in range(args.min_log2, args.max_log2 + 1):
                 n = 1 << lg
                 cold = n * 2.5 < 4 * 126e6
-                f = lambda: nf4.nf4_dequantize(packed, absmax, dq, n=n, blocksize=bs, out_dtype=dt, out=out)
-                for _ in range(3):
-                    f()
+                reps = 1
+                if args.method == "graph":
+                    reps = max(1, min(nmax // n, -(-int(4 * 126e6) // int(n * 2.5)))) if cold else 1
+
+                def f(r=0, stream=None):
+                    # copy r: elements [r*n, (r+1)*n) of the big buffers (disjoint, 256-B aligned)
+                    k0 = r * n
+                    if dq is not None:
+                        d = nf4.DQ(q[k0 // bs:(k0 + n) // bs], code2, a2[k0 // bs // 256:], 0.05)
+                        a = None
+                    else:
+                        d, a = None, absmax[k0 // bs:(k0 + n) // bs]
+                    nf4.nf4_dequantize(packed[k0 // 2:(k0 + n) // 2], a, d, n=n, blocksize=bs, out_dtype=dt,
+                                       out=out[k0:k0 + n], stream=stream)
+                for r in range(max(3, reps)):
+                    f(r % reps)
                 torch.cuda.synchronize()
-                times = []
-                for _ in range(args.reps):
-                    if cold:
-                        sink.copy_(flush.sum(dtype=torch.int64))
-                    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    s.record()
-                    f()
-                    e.record()
+                if args.method == "graph":
+                    K = args.launches
+                    gs = torch.cuda.Stream()
+                    gs.wait_stream(torch.cuda.current_stream())
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, stream=gs):
+                        for i in range(K):
+                            f(i % reps, gs)
+                    g.replay()
                     torch.cuda.synchronize()
-                    times.append(s.elapsed_time(e))
+                    times = []
+                    for _ in range(max(3, args.reps // 4)):
+                        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        s.record()
+                        g.replay()
+                        e.record()
+                        torch.cuda.synchronize()
+                        times.append(s.elapsed_time(e) / K)
+                    del g
+                else:
+                    times = []
+                    for _ in range(args.reps):
+                        if cold:
+                            sink.copy_(flush.sum(dtype=torch.int64))
+                        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        s.record()
+                        f()
+                        e.record()
+                        torch.cuda.synchronize()
+                        times.append(s.elapsed_time(e))
                 times.sort()
                 ms = times[len(times) // 2]
                 alg = n * wl.algorithmic_bytes_per_element(bs, args.dq)
                 gbs = alg / (ms * 1e-3) / 1e9
-                r = {"blocksize": bs, "dtype": dt, "n": n, "dq": args.dq, "cold": cold, "us": round(ms * 1e3, 2),
+                r = {"blocksize": bs, "dtype": dt, "n": n, "dq": args.dq, "cold": cold, "method": args.method,
+                     "rotating_copies": reps, "us": round(ms * 1e3, 2),
                      "gbs": round(gbs, 1), "frac_measured_copy": round(gbs / peak, 4),
                      "gelem_s": round(n / (ms * 1e-3) / 1e9, 1)}
                 rows.append(r)
