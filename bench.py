@@ -259,9 +259,13 @@ def run_reference(args, rank, world):
 # ---------------------------------------------------------------------------
 # work assignment and the cross-rank reduction (the only cross-rank traffic)
 # ---------------------------------------------------------------------------
-def rank_tensors(cfg: str, scaling: str, world: int, rank: int, layers=None):
+def rank_tensors(cfg: str, scaling: str, world: int, rank: int, layers=None, shard_of: int = 0):
     """Tensors rank `rank` dequantizes: its row shard of every weight (strong)
-    or a full linear-weight set of its own (weak)."""
+    or a full linear-weight set of its own (weak).  shard_of = S > 1 on one GPU:
+    rank 0's shard of an S-way split (one GPU's work of an S-GPU run, e.g.
+    config 4, whose full model does not fit one GPU)."""
+    if shard_of > 1 and world == 1:
+        return wl.config_tensors(cfg, world_size=shard_of, rank=0, layers=layers)
     if scaling == "strong":
         return wl.config_tensors(cfg, world_size=world, rank=rank, layers=layers)
     return wl.config_tensors(cfg, layers=layers)
@@ -321,7 +325,7 @@ def replicas_for(alg_bytes: int) -> int:
 def build_store(args, cfg, rank, world, device):
     from synth import stores
     c = wl.CONFIGS[cfg]
-    tensors = rank_tensors(cfg, args.scaling, world, rank, args.layers)
+    tensors = rank_tensors(cfg, args.scaling, world, rank, args.layers, args.shard_of)
     reps = replicas_for(alg_bytes_of(tensors, c.blocksize, c.dq))
     maker = stores.from_gaussian if args.inputs == "gaussian" else stores.from_hash
     return maker(tensors * reps, c.blocksize, c.dq, c.out_dtype, seed0=rank_seed0(cfg, rank), device=device), \
@@ -757,6 +761,7 @@ def run_ours(args, rank, world, local_rank):
                                                    f"(> 4 x L2), the {args.steps} timed steps launched back to back "
                                                    "from one CUDA graph (step i on copy i % copies); time = graph "
                                                    "replay / steps",
+                       "shard_of": args.shard_of or None,
                        "parallelism": (f"row-sharded {world} ways (each rank its own shard of every weight), "
                                        "no data-path collective" if args.scaling == "strong"
                                        else f"{world} independent replicas") if world > 1 else "single GPU"},
@@ -847,6 +852,8 @@ def main():
     ap.add_argument("--no-sol", action="store_true")
     ap.add_argument("--no-f1", action="store_true")
     ap.add_argument("--dry-run", action="store_true", help="no GPU: exercise the multi-rank harness with gloo")
+    ap.add_argument("--shard-of", type=int, default=0,
+                    help="N=1 only: time rank 0's row shard of an S-way split (config 4 per-GPU work)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-step-seconds", type=float, default=None,
                     help="oracle seconds per reference step (default: ~90 s / (steps + warmup), 0.2..5 s)")

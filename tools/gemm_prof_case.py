@@ -5,6 +5,8 @@ import paper_2604_02556_b200 as nf4
 from synth import stores
 from synth import workloads as wl
 M, N, K, S = 16, 21504, 5376, int(sys.argv[1]) if len(sys.argv) > 1 else 0
+if len(sys.argv) > 4:
+    M, N, K = (int(v) for v in sys.argv[2:5])
 ws = stores.from_hash([wl.Tensor("w", N, K)], 64, True, "bf16", 3, "cuda")
 e = ws.entries[0]
 dq = nf4.DQ(ws._ptr(ws.scales, e.scale_off), ws.code2.data_ptr(), ws._ptr(ws.groups, e.group_off), e.offset)

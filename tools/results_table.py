@@ -1,0 +1,118 @@
+#!/usr/bin/env python
+"""Round results table (profiles/r02_results.md) from committed measurements:
+bench lines, ncu launch lists, oracle rates and the full-parity log."""
+from __future__ import annotations
+
+import collections
+import csv
+import gzip
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+P = os.path.join(ROOT, "profiles")
+
+
+def jl(path):
+    with open(path) as f:
+        return [json.loads(l) for l in f if l.strip().startswith("{")]
+
+
+def ncu_gbs(path):
+    """Mean DRAM GB/s and bytes/algorithmic over the dequant launches of an ncu launch list."""
+    op = gzip.open if path.endswith(".gz") else open
+    with op(path, "rt") as f:
+        rows = list(csv.reader(f))
+    hi = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+    h = rows[hi]
+    ki, mi, vi, ii = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("ID")
+    per = collections.OrderedDict()
+    for r in rows[hi + 1:]:
+        if len(r) < len(h) or "dequant_kernel" not in r[ki]:
+            continue
+        per.setdefault(r[ii], {})[r[mi]] = float(r[vi].replace(",", ""))
+    b = sum(v["dram__bytes_read.sum"] + v["dram__bytes_write.sum"] for v in per.values())
+    t = sum(v["gpu__time_duration.sum"] for v in per.values())
+    return b / t if t else None, len(per)
+
+
+def main():
+    out = sys.argv[1] if len(sys.argv) > 1 else os.path.join(P, "r02_results.md")
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6550.0
+    main_line = jl(os.path.join(P, "r02_bench_default.json"))[-1]
+    par = jl(os.path.join(P, "r02_full_parity.jsonl"))
+    parity = collections.defaultdict(lambda: [0, 0])
+    for r in par:
+        parity[r["config"]][0] += r["elements_compared"]
+        parity[r["config"]][1] += r["mismatches"]
+    orc = {r["config"]: r for r in jl(os.path.join(P, "r02_oracle_rates.jsonl"))} if os.path.exists(
+        os.path.join(P, "r02_oracle_rates.jsonl")) else {}
+    ncu = {}
+    for cfg in ("cfg1", "cfg2", "cfg3", "cfg4"):
+        path = os.path.join(P, f"r02_ncu_launches_{cfg}.csv.gz")
+        if os.path.exists(path):
+            ncu[cfg] = ncu_gbs(path)
+    rows = []
+    m = main_line
+    rows.append(("cfg3 Qwen3-32B, DQ, fp16", 1, m["value"], m["gelem_per_s"], "cfg3"))
+    for k, d in m.get("extra_configs", {}).items():
+        rows.append((f"{k} " + {"cfg1": "4096x4096, fp32 absmax, fp16 (L2-cold, graph)",
+                                "cfg2": "Gemma-3-27B, DQ, bf16"}[k], 1, d["value"], d["gelem_per_s"], k))
+    cfg4p = os.path.join(P, "r02_bench_cfg4_shard.json")
+    if os.path.exists(cfg4p):
+        d = jl(cfg4p)[-1]
+        rows.append(("cfg4 Llama-3.3-70B, DQ, bf16: one GPU's row shard of 8", 1, d["value"], d["gelem_per_s"], "cfg4"))
+    lines = ["# Round 2 results (B200, 1 GPU per gpurun box)", "",
+             f"Peaks: measured HBM copy {peak} GB/s (MEASURED_PEAKS.json), nominal 8000 GB/s.  "
+             "GB/s = SURVEY 8(d) algorithmic bytes / time.  ncu = DRAM read+write bytes / kernel time over "
+             "the dequant launches of an ncu launch list (cold, serialised).  Parity = elements compared "
+             "with the oracle in `tests/test_full_parity_gpu.py` / mismatches.", "",
+             "| config | GPUs | GB/s | % nominal | % copy | Gelem/s | ncu DRAM GB/s | oracle Gelem/s (1 / T threads) | full parity (elements / mismatches) |",
+             "|---|---|---|---|---|---|---|---|---|"]
+    for name, g, v, ge, key in rows:
+        nc = ncu.get(key)
+        o = orc.get(key)
+        pr = parity.get(key)
+        ncu_cell = f"{nc[0]:.0f} ({nc[1]} launches)" if nc and nc[0] else "–"
+        orc_cell = (f"{o['gelem_per_s_1']:.3f} / {o['gelem_per_s_T']:.2f} ({o['threads']} threads)" if o else "–")
+        par_cell = f"{pr[0] / 1e9:.3g} G / {pr[1]}" if pr else "–"
+        lines.append(f"| {name} | {g} | {v:.0f} | {100 * v / 8000:.1f}% | {100 * v / peak:.1f}% | {ge:.0f} | "
+                     f"{ncu_cell} | {orc_cell} | {par_cell} |")
+    sw = os.path.join(P, "r02_sweep_cfg5_fp32absmax.jsonl")
+    swd = os.path.join(P, "r02_sweep_cfg5_dq.jsonl")
+    if os.path.exists(sw):
+        lines += ["", "Config 5 (one nf4_dequantize per size, graph-replayed, L2-cold below 4 x L2; "
+                      "fp16 shown, bf16 within 1%):", "",
+                  "| blocksize | absmax | 2^20 | 2^22 | 2^24 | 2^26 | 2^28 | 2^30 (GB/s, % copy) |", "|---|---|---|---|---|---|---|---|"]
+        for path, mode in ((sw, "fp32"), (swd, "DQ")):
+            if not os.path.exists(path):
+                continue
+            d = {(r["blocksize"], r["n"]): r for r in jl(path) if r["dtype"] == "f16"}
+            for bs in (64, 128, 256, 4096):
+                cells = []
+                for lg in (20, 22, 24, 26, 28, 30):
+                    r = d.get((bs, 1 << lg))
+                    cells.append(f"{r['gbs']:.0f} ({100 * r['frac_measured_copy']:.0f}%)" if r else "–")
+                lines.append(f"| {bs} | {mode} | " + " | ".join(cells) + " |")
+        c5 = parity.get("cfg5")
+        if c5:
+            lines += ["", f"Config 5 full parity: {c5[0] / 1e9:.1f} G elements, {c5[1]} mismatches."]
+    f1 = m.get("f1")
+    if f1:
+        lines += ["", f"F1 (fused NF4 dequant + tcgen05 GEMM), {f1['workload']}:", "",
+                  "| M | one launch ms | weights/s (T) | HBM frac | per-layer launches ms | dequant + cuBLAS ms | speed-up (one launch) |",
+                  "|---|---|---|---|---|---|---|"]
+        for k in ("M1", "M16", "M64"):
+            r = f1[k]
+            lines.append(f"| {k[1:]} | {r.get('one_launch_ms', '–')} | {r.get('one_launch_weights_per_s_T', '–')} | "
+                         f"{r.get('one_launch_hbm_frac', '–')} | {r['fused_ms']} | {r['unfused_ms']} | "
+                         f"{r.get('one_launch_speedup_vs_dequant_plus_cublas', '–')}x |")
+    with open(out, "w") as f:
+        f.write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+
+
+if __name__ == "__main__":
+    main()
