@@ -122,3 +122,13 @@ def test_alg_bytes_match_store_formula():
     assert bench.alg_bytes_of(t, 64, True) == 78_509_261_824      # 78.51 GB per Qwen3 step
     t = wl.config_tensors("cfg1")
     assert bench.alg_bytes_of(t, 64, False) == 42_991_616
+
+
+def test_shard_of_is_rank0_shard():
+    sys.path.insert(0, ROOT)
+    import bench
+    from synth import workloads as wl
+    a = bench.rank_tensors("cfg4", "strong", 1, 0, shard_of=8)
+    b = wl.config_tensors("cfg4", world_size=8, rank=0)
+    assert [(t.rows, t.cols) for t in a] == [(t.rows, t.cols) for t in b]
+    assert sum(t.n for t in a) * 8 == 68_451_041_280
