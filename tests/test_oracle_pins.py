@@ -618,3 +618,24 @@ def test_gemm_reference_linearity_and_magnitude(orc):
     pos = (syn.hash_packed(42, 0, N * K // 2) | 0x88).astype(np.uint8)
     yp, sp = orc.gemm_reference(b(np.abs(x1)), orc.OUT_BF16, pos, N, K, 64, absmax=absmax)
     assert np.array_equal(yp, sp)
+
+
+def test_oracle_memory_safe_under_asan_ubsan(tmp_path):
+    """the oracle built with -fsanitize=address,undefined, driven over
+    n = 1..1100 x blocksizes x modes x output types with exactly-sized buffers
+    and sub-range calls (tests/oracle_asan_driver.c): no sanitizer report, and
+    sub-range results equal the full-range result."""
+    import subprocess
+    here = os.path.dirname(os.path.abspath(__file__))
+    src = os.path.join(os.path.dirname(here), "oracle", "oracle.c")
+    exe = tmp_path / "oracle_asan"
+    cc = ["gcc", "-O1", "-g", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fsanitize=address,undefined",
+          "-fno-sanitize-recover=all", "-o", str(exe), src, os.path.join(here, "oracle_asan_driver.c")]
+    r = subprocess.run(cc, capture_output=True, text=True)
+    if r.returncode != 0 and "sanitize" in r.stderr:
+        pytest.skip("gcc sanitizer runtime unavailable: " + r.stderr[-200:])
+    assert r.returncode == 0, r.stderr[-2000:]
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, ASAN_OPTIONS="detect_leaks=1:abort_on_error=1"))
+    assert r.returncode == 0, (r.stdout + r.stderr)[-3000:]
+    assert "0 failures" in r.stdout
