@@ -1264,9 +1264,17 @@ extern "C" int64_t nf4_gemm_grouped_workspace_bytes(int32_t M, const int32_t* N,
 
 extern "C" int64_t nf4_gemm_multi_workspace_bytes(int32_t M, const int32_t* N, const int32_t* K, int32_t count) {
   if (M <= 0 || !N || !K || count <= 0 || count > NF4_GEMM_MAX_MULTI) return 0;
-  for (int i = 0; i < count; ++i)
-    if (N[i] < 0 || K[i] <= 0 || K[i] % 64 != 0) return 0;
-  const int64_t b = streamk_ws_bytes(M, N, K, count);
+  // problems with no work (N == 0 or K == 0) take no tiles, exactly as nf4_gemm_multi skips them
+  int32_t n[NF4_GEMM_MAX_MULTI], k[NF4_GEMM_MAX_MULTI];
+  int c = 0;
+  for (int i = 0; i < count; ++i) {
+    if (N[i] < 0 || K[i] < 0 || K[i] % 64 != 0) return 0;
+    if (N[i] == 0 || K[i] == 0) continue;
+    n[c] = N[i];
+    k[c++] = K[i];
+  }
+  if (c == 0) return 0;
+  const int64_t b = streamk_ws_bytes(M, n, k, c);
   return b > 0 ? b : 0;
 }
 
@@ -1320,25 +1328,37 @@ static nf4_status gemm_run(nf4_dtype x_dtype, int32_t M, int32_t blocksize, cons
       if ((mem_in[i].absmax == nullptr) == (mem_in[i].dq == nullptr)) return NF4_ERR_BAD_STATE;
       if (mem_in[i].dq && mem_in[i].dq->blocksize2 != 256) return NF4_ERR_BAD_STATE;
       if (mem_in[i].K % 64 != 0 || mem_in[i].K % blocksize != 0) return NF4_ERR_BAD_SIZE;
+      if (M > 0 && mem_in[i].N > 0) {   // K == 0: Y = 0 is written
+        if (!mem_in[i].y) return NF4_ERR_NULL_POINTER;
+        if (!aligned(mem_in[i].y, y_dtype == NF4_F32 ? 4 : 2)) return NF4_ERR_MISALIGNED;
+      }
       continue;
     }
     const nf4_status st = check_member(mem_in[i], y_dtype, blocksize);
     if (st != NF4_OK) return st;
   }
-  // problems with N == 0 or K == 0 contribute no tiles (K == 0 with N > 0: Y = 0)
+  // problems with N == 0 or K == 0 contribute no tiles (K == 0 with N > 0: Y = 0,
+  // written after every argument has been validated)
   HostMember mem[kMaxMembers];
-  int nmem = 0;
+  int nmem = 0, nzero = 0;
   for (int i = 0; i < count; ++i) {
     if (M == 0 || mem_in[i].N == 0) continue;
-    if (mem_in[i].K == 0) {
-      const size_t bytes = size_t(M) * mem_in[i].N * (y_dtype == NF4_F32 ? 4 : 2);
-      if (cudaMemsetAsync(mem_in[i].y, 0, bytes, static_cast<cudaStream_t>(stream)) != cudaSuccess)
-        return NF4_ERR_CUDA;
-      continue;
-    }
+    if (mem_in[i].K == 0) { ++nzero; continue; }
     mem[nmem++] = mem_in[i];
   }
-  if (nmem == 0) { set_launch_count(0); return NF4_OK; }
+  auto zero_fill = [&]() -> bool {
+    for (int i = 0; i < count && nzero > 0; ++i)
+      if (M > 0 && mem_in[i].N > 0 && mem_in[i].K == 0 &&
+          cudaMemsetAsync(mem_in[i].y, 0, size_t(M) * mem_in[i].N * (y_dtype == NF4_F32 ? 4 : 2),
+                          static_cast<cudaStream_t>(stream)) != cudaSuccess)
+        return false;
+    return true;
+  };
+  if (nmem == 0) {
+    if (!zero_fill()) { cudaGetLastError(); return NF4_ERR_CUDA; }
+    set_launch_count(0);
+    return NF4_OK;
+  }
   const int bn = pick_bn(M);
   int32_t Ns[kMaxMembers], Ks[kMaxMembers];
   for (int i = 0; i < nmem; ++i) { Ns[i] = mem[i].N; Ks[i] = mem[i].K; }
@@ -1437,6 +1457,7 @@ static nf4_status gemm_run(nf4_dtype x_dtype, int32_t M, int32_t blocksize, cons
       return NF4_ERR_CUDA;
     }
   }
+  if (!zero_fill()) { cudaGetLastError(); return NF4_ERR_CUDA; }
   cudaError_t e;
   switch (bn) {
     case 16: e = bf16 ? launch<16, true>(p, maps, grid, s) : launch<16, false>(p, maps, grid, s); break;

@@ -170,3 +170,37 @@ def test_package_code2_table_equals_test_input_table():
     a, b = bnb_dynamic_code2(), syn.dynamic_map_code2()
     assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
     assert a[127] == 0.0 and a[255] == 1.0 and np.all(np.diff(a) > 0)
+
+
+def test_gemm_multi_validation_without_gpu(lib):
+    """nf4_gemm_multi validates every problem before any CUDA call."""
+    P = ctypes.c_void_p
+    fake = P(0x1000)
+    from paper_2604_02556_b200._lib import GemmProblem
+    pr = (GemmProblem * 65)()
+    for q in pr:
+        q.x, q.K, q.packed, q.absmax, q.N, q.y = fake, 256, fake, fake, 128, fake
+    assert lib.nf4_gemm_multi(pr, 0, 4, 1, 64, 1, None, 0, None) == 2       # count < 1
+    assert lib.nf4_gemm_multi(pr, 65, 4, 1, 64, 1, None, 0, None) == 2      # count > NF4_GEMM_MAX_MULTI
+    assert lib.nf4_gemm_multi(None, 2, 4, 1, 64, 1, None, 0, None) == 1     # NULL table
+    assert lib.nf4_gemm_multi(pr, 2, 4, 2, 64, 1, None, 0, None) == 4       # x dtype fp32
+    pr[1].K = 96                                                             # K not a multiple of 64
+    assert lib.nf4_gemm_multi(pr, 2, 4, 1, 64, 1, None, 0, None) == 2
+    pr[1].K = 128
+    assert lib.nf4_gemm_multi(pr, 2, 4, 1, 256, 1, None, 0, None) == 2      # K not a multiple of blocksize
+    pr[1].x = P(0x1008)                                                      # X not 16-byte aligned
+    assert lib.nf4_gemm_multi(pr, 2, 4, 1, 64, 1, None, 0, None) == 5
+    pr[1].x = None
+    assert lib.nf4_gemm_multi(pr, 2, 4, 1, 64, 1, None, 0, None) == 1
+    pr[1].x = fake
+    pr[1].K = 0                                                              # K == 0: Y = 0, y still required
+    pr[1].y = None
+    assert lib.nf4_gemm_multi(pr, 2, 4, 1, 64, 1, None, 0, None) == 1
+    # workspace sizing skips problems without work, as the call does
+    N = (ctypes.c_int32 * 3)(128, 0, 256)
+    K = (ctypes.c_int32 * 3)(512, 512, 0)
+    N1 = (ctypes.c_int32 * 1)(128)
+    K1 = (ctypes.c_int32 * 1)(512)
+    assert lib.nf4_gemm_multi_workspace_bytes(4, N, K, 3) == lib.nf4_gemm_multi_workspace_bytes(4, N1, K1, 1)
+    K[0] = 100
+    assert lib.nf4_gemm_multi_workspace_bytes(4, N, K, 3) == 0
