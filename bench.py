@@ -579,6 +579,13 @@ def f1_layer_groups(tensors):
     return groups
 
 
+# The fused GEMM's own bound: one shared-memory table lookup per weight costs 1/32 of a
+# 128-B LSU data-pipe wavefront (16-entry table: LDS.32 per weight; byte-pair table:
+# LDS.64 per two weights -- the same wavefronts), and that pipe sustains 6.48 T
+# lookups/s on this GPU (tools/lutbench.cu, profiles/r01_lutbench.txt).
+F1_LUT_BOUND = 6.48e12
+
+
 def measure_f1(nf4, torch, peak, ms_list=(1, 16, 64), layers=8, steps=20, warmup=5):
     """Y_t = X_t . W_t^T for every linear weight of `layers`
     Gemma-3-27B decoder layers (DQ NF4, bf16 X/Y), fused vs the unfused path the
@@ -599,7 +606,11 @@ def measure_f1(nf4, torch, peak, ms_list=(1, 16, 64), layers=8, steps=20, warmup
     n_total = sum(t.n for t in tensors)
     out = {"workload": f"Gemma-3-27B, {layers} decoder layers x 7 linear weights ({n_total / 1e9:.2f} G NF4 "
                        f"weights, blocksize 64, double-quant), bf16 X and Y",
-           "launches_per_step": len(groups), "steps": steps}
+           "launches_per_step": len(groups), "steps": steps,
+           "roofline_note": "hbm_frac: bytes the fused step must move (codes + scales + X + Y) / time / measured "
+                            "copy peak; lut_bound_frac: weights/s / 6.48 T lookups/s, the measured rate of the "
+                            "shared-memory LSU data pipe for one table lookup per weight (the fused kernel's "
+                            "binding pipe, ncu: l1tex ~80% busy in the one-launch step)"}
     wbuf = torch.empty(max(t.n for t in tensors), dtype=torch.bfloat16, device="cuda")
     for M in ms_list:
         xs = {}
@@ -667,8 +678,10 @@ def measure_f1(nf4, torch, peak, ms_list=(1, 16, 64), layers=8, steps=20, warmup
                         "tflops": round(2.0 * M * n_total / (f_ms * 1e-3) / 1e12, 2),
                         "hbm_gbs": round(gbs, 1), "hbm_frac": round(gbs / peak, 4),
                         "bytes_per_step": wbytes + xybytes}
+        out[f"M{M}"]["lut_bound_frac"] = round(n_total / (f_ms * 1e-3) / F1_LUT_BOUND, 4)
         if o_ms is not None:
             gbs1 = (wbytes + xybytes) / (o_ms * 1e-3) / 1e9
+            out[f"M{M}"]["one_launch_lut_bound_frac"] = round(n_total / (o_ms * 1e-3) / F1_LUT_BOUND, 4)
             out[f"M{M}"].update({"one_launch_ms": round(o_ms, 4),
                                  "one_launch_speedup_vs_dequant_plus_cublas": round(u_ms / o_ms, 3),
                                  "one_launch_weights_per_s_T": round(n_total / (o_ms * 1e-3) / 1e12, 3),
