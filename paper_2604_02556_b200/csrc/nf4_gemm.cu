@@ -1128,7 +1128,7 @@ static bool make_map(CUtensorMap* m, CUtensorMapDataType dt, int elem, const voi
     int dt, sw;
     CUtensorMap map;
   };
-  constexpr int kCache = 64;
+  constexpr int kCache = 256;   // a 64-problem nf4_gemm_multi call needs up to 128 maps
   thread_local Entry cache[kCache] = {};
   const uint64_t h = (reinterpret_cast<uintptr_t>(base) >> 8) ^ (cols * 0x9E3779B97F4A7C15ull) ^ (rows << 7) ^
                      (uint64_t(box_rows) << 3) ^ uint64_t(dt);
