@@ -464,6 +464,7 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
   __shared__ __align__(8) uint64_t c_full[CST], x_full[CST], c_free[CST], w_full[S], a_free[S], acc_full[NACC],
       acc_empty[NACC];
   __shared__ uint32_t tmem_holder;
+  __shared__ int epi_done[NACC];                              // epilogue warps finished, per accumulator
   __shared__ int sk_range[3];                                 // stream-K: range start, end, first slot
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* ptab = smem;                                       // NF4_GEMM_PAIR: 256 rows x 32 lanes x 8 B
@@ -501,6 +502,7 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
     for (int s = 0; s < NACC; ++s) {
       mbar_init(&acc_full[s], 1);
       mbar_init(&acc_empty[s], kProducerWarps);
+      epi_done[s] = 0;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (p.streamk) {
@@ -626,6 +628,17 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
         const int cs = Jg % CST;
         const int slot = Jg % S;
         const uint32_t aph = uint32_t(Jg / S) & 1u;
+        // Parity waits see one phase back: c_full[cs] may only be polled for stage Jg once
+        // stage Jg - CST (its previous use) has landed.  The previous stage of this group
+        // (Jg - G) waited for the MMA to consume Jg - G - S, which covers it when
+        // CST >= G + S; otherwise first wait for the MMA to have consumed Jg - CST (its
+        // slot's barrier is safe to poll: Jg - CST - S <= Jg - G - S since CST >= G).
+        if constexpr (CST < G + S) {
+          if (Jg >= CST) {
+            const int Jp = Jg - CST;
+            mbar_wait_parity(&a_free[Jp % S], uint32_t(Jp / S) & 1u);
+          }
+        }
         mbar_wait_parity(&c_full[cs], uint32_t(Jg / CST) & 1u);   // codes of this super-stage landed
         if (wl == 0 && lane == 0) NF4_TRACE_J(100, Jg);
         const int64_t b0 = blk_base + kc0 + SUB * j;
@@ -772,6 +785,21 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
       const int jlast = J + (nsuper > 0 ? nsuper - 1 : 0);
       if (jlast % G == g) {
         const int ab = sidx % NACC;
+        // acc_full[ab] may only be polled for segment sidx once the previous segment on
+        // this accumulator (sidx - NACC) has been committed: a group can be several short
+        // segments ahead of the MMA, and a parity wait sees one phase back.  That
+        // segment's epilogue waited for its commit, so wait for the epilogue (a monotone
+        // count of finished epilogue warps per accumulator: no phase ambiguity).
+        if (sidx >= NACC) {
+          const int need = (sidx / NACC) * kProducerWarps;
+          while (true) {
+            int v;
+            asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(&epi_done[ab]))
+                         : "memory");
+            if (v >= need) break;
+            __nanosleep(32);
+          }
+        }
         mbar_wait_parity(&acc_full[ab], uint32_t(sidx / NACC) & 1u);
         asm volatile("griddepcontrol.wait;" ::: "memory");   // y / partials / counters: the previous kernel is done
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -812,7 +840,10 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
         }
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
-        if (lane == 0) mbar_arrive(&acc_empty[ab]);     // the MMA may reuse this accumulator
+        if (lane == 0) {
+          mbar_arrive(&acc_empty[ab]);                   // the MMA may reuse this accumulator
+          asm volatile("red.release.cta.shared::cta.add.u32 [%0], 1;" ::"r"(smem_u32(&epi_done[ab])) : "memory");
+        }
         if (p.streamk && !direct && sg.kc0 + nk < sg.nkt) {
           // a non-final piece: publish (release) -- the tile's last CTA sums it at its end
           __threadfence();

@@ -550,3 +550,21 @@ def test_gemm_multi_many_problems_and_errors(nf4, orc):
     with pytest.raises(nf4.NF4Error) as e:
         nf4.nf4_gemm_multi(probs + probs[:9], M=M)
     assert e.value.status == 2
+
+
+@pytest.mark.parametrize("K", [64, 128, 256])
+@pytest.mark.parametrize("M", [1, 16, 40])
+def test_gemm_many_short_segments_per_cta(nf4, orc, M, K):
+    """Small K (1-4 chunks per tile) and many tiles: every CTA's stream-K range
+    holds several whole tiles, i.e. several short segments back to back, so the
+    two TMEM accumulators are reused while earlier segments may still be in the
+    MMA pipe.  Exact sums (sparse +-1 X) must come out bit for bit."""
+    N = 128 * 148 * 4 + 64
+    for dq in (False, True):
+        packed, kw = _weights(N, K, 64, dq, seed=M * 7 + K + int(dq))
+        x16 = _to16(_sparse_pm1(M, K, min(K, 64), M + K + 1), "bf16")
+        ref = _exact_reference(x16, "bf16", packed, N, K, 64, kw, orc)
+        for _ in range(2):
+            y = _run(nf4, x16, "bf16", M, packed, kw, N, K, 64, "f32", 0).cpu().numpy()
+            bad = _pos0(y) != _pos0(ref.astype(np.float32))
+            assert not bad.any(), (M, K, dq, int(bad.sum()), np.argwhere(bad)[:3].tolist())
