@@ -568,3 +568,34 @@ def test_gemm_many_short_segments_per_cta(nf4, orc, M, K):
             y = _run(nf4, x16, "bf16", M, packed, kw, N, K, 64, "f32", 0).cpu().numpy()
             bad = _pos0(y) != _pos0(ref.astype(np.float32))
             assert not bad.any(), (M, K, dq, int(bad.sum()), np.argwhere(bad)[:3].tolist())
+
+
+STRESS = [  # (M, N, K, blocksize): every token-tile width, ragged N and M, K from 1 chunk up
+    (17, 1000, 192, 64), (33, 777, 320, 64), (65, 300, 448, 64), (129, 520, 640, 128), (257, 256, 256, 256),
+    (300, 384, 128, 64), (3, 20000, 64, 64), (48, 9000, 128, 128), (100, 5000, 192, 64), (200, 2000, 4096, 4096),
+]
+
+
+@pytest.mark.parametrize("M,N,K,bs", STRESS)
+def test_gemm_shape_stress_exact(nf4, orc, M, N, K, bs):
+    """Odd shapes through stream-K, the classic split grid and nf4_gemm_multi:
+    partial super-stages, ragged tiles, several token tiles, small and large K,
+    general-blocksize scales -- Y exact (sparse +-1 X) in every mode."""
+    import torch
+    dq = (M + N) % 2 == 0
+    packed, kw = _weights(N, K, bs, dq, seed=M * 31 + N + K)
+    x16 = _to16(_sparse_pm1(M, K, min(K, 64), M * 3 + K), "bf16")
+    ref = _pos0(_exact_reference(x16, "bf16", packed, N, K, bs, kw, orc).astype(np.float32))
+    for splits in (0, 1, 3):
+        y = _run(nf4, x16, "bf16", M, packed, kw, N, K, bs, "f32", splits).cpu().numpy()
+        assert np.array_equal(_pos0(y), ref), (M, N, K, bs, splits)
+    x = _x_tensor(x16, "bf16", M, K)
+    if dq:
+        prob = (x, K, dev(packed), None, nf4.DQ(dev(kw["qabsmax"]), dev(kw["code2"]), dev(kw["absmax2"]),
+                                               kw["offset"]), N)
+    else:
+        prob = (x, K, dev(packed), dev(kw["absmax"]), None, N)
+    ys = nf4.nf4_gemm_multi([prob, prob], M=M, blocksize=bs, y_dtype="f32")
+    torch.cuda.synchronize()
+    for y in ys:
+        assert np.array_equal(_pos0(y.cpu().numpy()), ref), (M, N, K, bs, "multi")
