@@ -68,6 +68,9 @@ namespace gemm {
 // group that ran ahead start its next super-stage before the in-order MMA has
 // consumed its previous one (it waits only for the slot's previous occupant).
 // TMEM: NACC x 32 accumulator columns + SLOTS x SUB x 32 A columns <= 512.
+#ifndef NF4_GEMM_ACC_GUARD
+#define NF4_GEMM_ACC_GUARD 1
+#endif
 #ifndef NF4_GEMM_W4_SLOTS
 #define NF4_GEMM_W4_SLOTS 7
 #endif
@@ -144,10 +147,22 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 #endif
 // 0: try_wait with a 10 ms suspend hint; 1: try_wait (hardware default time
 // limit); 2: test_wait spin; >2: try_wait + __nanosleep(mode) between polls.
+#ifndef NF4_GEMM_HANG_DIAG
+#define NF4_GEMM_HANG_DIAG 0   // diagnostics builds only: report and trap a wait that never completes
+#endif
 __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
   const uint32_t b = smem_u32(bar);
   uint32_t done = 0;
+#if NF4_GEMM_HANG_DIAG
+  long long spins = 0;
+#endif
   while (!done) {
+#if NF4_GEMM_HANG_DIAG
+    if (++spins == (1ll << 24)) {
+      printf("HANG cta %d warp %d lane %d bar_smem 0x%x parity %u\n", int(blockIdx.x), int(threadIdx.x >> 5),
+             int(threadIdx.x & 31), b, parity);
+    }
+#endif
 #if NF4_GEMM_WAIT_MODE == 0
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -456,6 +471,10 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
   constexpr int A0 = NACC * ACC;
   constexpr int S = slots_for<BN>();   // A-tile slots: super-stage Jg uses slot Jg % S
   static_assert(S >= G, "a group's previous fill must have freed the slot's previous-but-one use");
+  static_assert(CST >= S, "the A-slot wait must prove the code slot's previous use landed");
+  // first piece of a stage dequantized before the A-slot wait only when that keeps every
+  // c_full wait within one phase (see the producers)
+  constexpr bool kEarlyFirstPiece = CST >= G + S;
   static_assert(A0 + S * SUB * 32 <= 512, "TMEM budget");
   constexpr int kSuperCodeBytes = 128 * SUB * kCodeBytes;
   constexpr int kSuperXBytes = SUB * BN * kRowBytes;
@@ -489,6 +508,12 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
       *reinterpret_cast<float4*>(ptab + 16 * i) = make_float4(h, l, h, l);
     }
   }
+#if NF4_GEMM_HANG_DIAG
+  if (threadIdx.x == 0 && blockIdx.x == 0)
+    printf("BARS c_full 0x%x x_full 0x%x c_free 0x%x w_full 0x%x a_free 0x%x acc_full 0x%x acc_empty 0x%x CST %d S %d G %d\n",
+           smem_u32(c_full), smem_u32(x_full), smem_u32(c_free), smem_u32(w_full), smem_u32(a_free),
+           smem_u32(acc_full), smem_u32(acc_empty), CST, S, G);
+#endif
   if (threadIdx.x == 0) {
     for (int s = 0; s < CST; ++s) {
       mbar_init(&c_full[s], 1);
@@ -628,16 +653,17 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
         const int cs = Jg % CST;
         const int slot = Jg % S;
         const uint32_t aph = uint32_t(Jg / S) & 1u;
-        // Parity waits see one phase back: c_full[cs] may only be polled for stage Jg once
-        // stage Jg - CST (its previous use) has landed.  The previous stage of this group
-        // (Jg - G) waited for the MMA to consume Jg - G - S, which covers it when
-        // CST >= G + S; otherwise first wait for the MMA to have consumed Jg - CST (its
-        // slot's barrier is safe to poll: Jg - CST - S <= Jg - G - S since CST >= G).
-        if constexpr (CST < G + S) {
-          if (Jg >= CST) {
-            const int Jp = Jg - CST;
-            mbar_wait_parity(&a_free[Jp % S], uint32_t(Jp / S) & 1u);
-          }
+        // A parity wait must be made while the barrier is within one phase of the awaited
+        // one, on both sides.  c_full[cs] for stage Jg needs stage Jg - CST (its previous
+        // use) landed.  With CST >= G + S this group's previous stage (which waited for the
+        // MMA to consume Jg - G - S) proves it, and the first piece of the stage can be
+        // dequantized before waiting for the A slot.  Otherwise the A-slot wait (the MMA
+        // consumed Jg - S; CST >= S) comes first.  (Waiting for the consumption of Jg - CST
+        // itself is NOT safe: its slot may already be two uses further, and the wait would
+        // then block until a stage this group has yet to produce.)
+        if constexpr (!kEarlyFirstPiece) {
+          mbar_wait_parity(&a_free[slot], aph ^ 1u);     // the MMA is done with the slot's previous tiles
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         }
         mbar_wait_parity(&c_full[cs], uint32_t(Jg / CST) & 1u);   // codes of this super-stage landed
         if (wl == 0 && lane == 0) NF4_TRACE_J(100, Jg);
@@ -694,7 +720,7 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
                   // the A tiles (a warp that ran ahead of its group keeps working).
                   constexpr int kWords = 16 / (NF4_GEMM_ST_SPLIT ? NF4_GEMM_ST_SPLIT : 1), kCc = kWords / 4;
                   if (cc % kCc == kCc - 1) {
-                    if (first && cc == kCc - 1) {
+                    if (kEarlyFirstPiece && first && cc == kCc - 1) {
                       mbar_wait_parity(&a_free[slot], aph ^ 1u);        // the MMA is done with our previous A tiles
                       if (wl == 0 && lane == 0) NF4_TRACE_J(200, Jg);
                       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -746,7 +772,7 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
                     }
                   }
                 }
-                if (first) {
+                if (kEarlyFirstPiece && first) {
                   mbar_wait_parity(&a_free[slot], aph ^ 1u);              // the MMA is done with our previous A tiles
                   if (wl == 0 && lane == 0) NF4_TRACE_J(200, Jg);
                   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -790,7 +816,7 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
         // segments ahead of the MMA, and a parity wait sees one phase back.  That
         // segment's epilogue waited for its commit, so wait for the epilogue (a monotone
         // count of finished epilogue warps per accumulator: no phase ambiguity).
-        if (sidx >= NACC) {
+        if (NF4_GEMM_ACC_GUARD && sidx >= NACC) {
           const int need = (sidx / NACC) * kProducerWarps;
           while (true) {
             int v;
