@@ -545,3 +545,34 @@ def test_host_buffer_batched_mixed_fp32_and_dq_small_blocks(nf4, orc):
         nf4.nf4_dequantize_host_batched(descs, "bf16", workspace=ws, chunk_elems=chunk)
         for d, ref in zip(descs, refs):
             assert np.array_equal(d.out.numpy().view(np.uint16), ref)
+
+
+def test_quarter_tile_launches(nf4, orc):
+    """Launches below 4 waves of default tiles use 4096-element tiles: single
+    tensors around the threshold and decoder-layer-sized batches (<= 16 tensors)
+    of ragged, mixed-mode, mixed-blocksize tensors give the oracle's bytes."""
+    import torch
+    sm = torch.cuda.get_device_properties(0).multi_processor_count
+    edge = 4 * sm * TILE
+    for n in (edge - TILE - 4097, edge - 1, edge, edge + 3 * 4096 + 5, 3 * 4096 + 17):
+        packed, kw = _inputs(n, 64, n % 2 == 0, n % 1000)
+        got = host16(_gpu_deq(nf4, packed, kw, n, 64, "f16"))
+        assert np.array_equal(got, _oracle(orc, packed, kw, n, 64, "f16")), n
+    rng = np.random.Generator(np.random.Philox(9))
+    descs, refs = [], []
+    for i in range(12):
+        n = int(rng.integers(1, 40 * 4096))
+        bs = int([64, 128, 256, 4096][i % 4])
+        dq = bool(i % 3 == 1)
+        packed, kw = _inputs(n, bs, dq, 3000 + i)
+        out = torch.zeros(n, dtype=torch.bfloat16, device="cuda")
+        if dq:
+            d = nf4.DQ(dev(kw["qabsmax"]), dev(kw["code2"]), dev(kw["absmax2"]), kw["offset"])
+            descs.append(nf4.NF4Tensor(dev(packed), n, bs, out, None, d))
+        else:
+            descs.append(nf4.NF4Tensor(dev(packed), n, bs, out, dev(kw["absmax"]), None))
+        refs.append(_oracle(orc, packed, kw, n, bs, "bf16"))
+    nf4.nf4_dequantize_batched(descs, "bf16")
+    torch.cuda.synchronize()
+    for d, ref in zip(descs, refs):
+        assert np.array_equal(host16(d.out), ref)
