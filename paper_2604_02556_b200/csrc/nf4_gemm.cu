@@ -242,7 +242,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #ifndef NF4_GEMM_DIAG
 #define NF4_GEMM_DIAG 0
 #endif
-#define NF4_EXP(bit) (NF4_GEMM_DIAG && (p.experiment & (bit)))
+// NF4_GEMM_EXP_CONST: the same pipeline-skipping experiments fixed at compile time, so
+// the rest of the kernel is the production code (tools/: bound attribution).
+#ifndef NF4_GEMM_EXP_CONST
+#define NF4_GEMM_EXP_CONST 0
+#endif
+#define NF4_EXP(bit) ((NF4_GEMM_EXP_CONST & (bit)) || (NF4_GEMM_DIAG && (p.experiment & (bit))))
 #define NF4_TRACING (NF4_GEMM_DIAG && p.trace != nullptr)
 // per-super-stage event times of CTA 0, slot base + J (J < 80)
 #define NF4_TRACE_J(base, Jv)                                                                       \
