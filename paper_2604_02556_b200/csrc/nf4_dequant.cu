@@ -69,6 +69,8 @@ static const Variant kVariants[] = {
     {"v2u4xc", 8, 4, false, false, true, true},      // 10
     {"v2u4sxcd", 8, 4, false, true, true, true},     // 11: + double-buffered scale cache / CLC slots
     {"v2u4sxcp", 8, 4, false, true, true, true},     // 12: v2u4sxc + byte-pair table (32 KB smem per CTA)
+    {"v2u2sxc", 8, 2, false, true, true, true},      // 13: v2u4sxc with 8192-element tiles
+    {"v2u4sxcw", 8, 4, false, true, true, true},     // 14: v2u4sxc with write-back (default-policy) stores
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 constexpr int kDefaultVariant = 8;   // v2u4sxc: best measured on B200 (profiles/r01_variants.md)
@@ -215,12 +217,14 @@ __device__ __forceinline__ void decode_group_pair(uint32_t ptab_lane, const Code
   }
 }
 
-template <int NW>
+// STH 0: evict-first streaming stores (.cs); 1: default write-back policy
+template <int NW, int STH = 0>
 __device__ __forceinline__ void st_group(void* out, const uint32_t (&w)[NW]) {
 #pragma unroll
   for (int h = 0; h < NW / 8; ++h) {
     const uint32_t(&ww)[8] = *reinterpret_cast<const uint32_t(*)[8]>(&w[8 * h]);
-    st_out_v8(static_cast<uint8_t*>(out) + 32 * h, ww);
+    if constexpr (STH == 0) st_out_v8(static_cast<uint8_t*>(out) + 32 * h, ww);
+    else st_out_v8_wb(static_cast<uint8_t*>(out) + 32 * h, ww);
   }
 }
 
@@ -284,7 +288,7 @@ __device__ __forceinline__ int64_t clc_result(const uint4* result) {
 }
 
 template <int OUT, int VEC, int U, bool PERSIST, bool SSCALE, bool PRMT, bool CLC, bool DB = false,
-          int MAXB = NF4_MAX_BATCH, bool EARLY = false, bool PAIR = false>
+          int MAXB = NF4_MAX_BATCH, bool EARLY = false, bool PAIR = false, int STH = 0>
 __global__ void __launch_bounds__(kThreads) dequant_kernel(const __grid_constant__ BatchParamsT<MAXB> P) {
   constexpr int GROUP = 2 * VEC;                      // elements per thread-group
   constexpr int64_t TILE = int64_t(kThreads) * GROUP * U;
@@ -392,7 +396,7 @@ __global__ void __launch_bounds__(kThreads) dequant_kernel(const __grid_constant
             decode_group_pair<OUT, VEC>(ptab_lane, q[u], a[u], w);
           else
             decode_group<OUT, VEC, PRMT>(lut, q[u], a[u], w);
-          st_group(out_at<OUT>(d.out, e0), w);
+          st_group<OutWords<OUT, VEC>::value, STH>(out_at<OUT>(d.out, e0), w);
         }
       } else {
         for (int u = 0; u < U; ++u) {
@@ -442,6 +446,8 @@ static KernelFn kernel_for(int v) {
     case 9: return dequant_kernel<OUT, 8, 4, false, false, false, true>;
     case 10: return dequant_kernel<OUT, 8, 4, false, false, true, true>;
     case 12: return dequant_kernel<OUT, 8, 4, false, true, true, true, false, NF4_MAX_BATCH, false, true>;
+    case 13: return dequant_kernel<OUT, 8, 2, false, true, true, true>;
+    case 14: return dequant_kernel<OUT, 8, 4, false, true, true, true, false, NF4_MAX_BATCH, false, false, 1>;
     default: return dequant_kernel<OUT, 8, 4, false, true, true, true, true>;
   }
 }

@@ -54,6 +54,13 @@ __device__ __forceinline__ void st_out_v8(void* p, const uint32_t (&w)[8]) {
                : "memory");
 }
 
+// 256-bit store with the default (write-back) cache policy.
+__device__ __forceinline__ void st_out_v8_wb(void* p, const uint32_t (&w)[8]) {
+  asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(w[0]),
+               "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+               : "memory");
+}
+
 // Pack two fp32 into 16-bit pair with RNE.  `lo` lands in bits [0,16) -- the
 // earlier element (high nibble, R2) -- and `hi` in bits [16,32).  PTX
 // cvt.rn.{f16x2,bf16x2}.f32 d, a, b puts a in the upper half.
