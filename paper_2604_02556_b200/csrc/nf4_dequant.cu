@@ -71,6 +71,8 @@ static const Variant kVariants[] = {
     {"v2u4sxcp", 8, 4, false, true, true, true},     // 12: v2u4sxc + byte-pair table (32 KB smem per CTA)
     {"v2u2sxc", 8, 2, false, true, true, true},      // 13: v2u4sxc with 8192-element tiles
     {"v2u4sxcw", 8, 4, false, true, true, true},     // 14: v2u4sxc with write-back (default-policy) stores
+    {"v2u4sxcf", 8, 4, false, true, true, true},     // 15: v2u4sxc + L2 prefetch of the scales one wave ahead
+    {"v2u4sxcF", 8, 4, false, true, true, true},     // 16: v2u4sxc + L2 prefetch of scales and codes one wave ahead
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 constexpr int kDefaultVariant = 8;   // v2u4sxc: best measured on B200 (profiles/r01_variants.md)
@@ -103,7 +105,7 @@ template <int MAXB>
 struct BatchParamsT {
   int64_t total_tiles;
   int32_t count;
-  int32_t pad_;
+  int32_t prefetch_ahead; // PF variants: L2-prefetch the inputs of tile + prefetch_ahead (0: off)
   float lut[16];          // the 16-entry codebook (NF4 unless nf4_dequantize_ex supplies one)
   TensorDesc t[MAXB];
 };
@@ -288,7 +290,7 @@ __device__ __forceinline__ int64_t clc_result(const uint4* result) {
 }
 
 template <int OUT, int VEC, int U, bool PERSIST, bool SSCALE, bool PRMT, bool CLC, bool DB = false,
-          int MAXB = NF4_MAX_BATCH, bool EARLY = false, bool PAIR = false, int STH = 0>
+          int MAXB = NF4_MAX_BATCH, bool EARLY = false, bool PAIR = false, int STH = 0, int PF = 0>
 __global__ void __launch_bounds__(kThreads) dequant_kernel(const __grid_constant__ BatchParamsT<MAXB> P) {
   constexpr int GROUP = 2 * VEC;                      // elements per thread-group
   constexpr int64_t TILE = int64_t(kThreads) * GROUP * U;
@@ -348,6 +350,33 @@ __global__ void __launch_bounds__(kThreads) dequant_kernel(const __grid_constant
       const TensorDesc& d = P.t[cur];
       const int64_t first = cur == 0 ? 0 : P.t[cur - 1].tile_end;
       const int64_t e_tile = (tile - first) * TILE;
+      if (PF > 0 && P.prefetch_ahead > 0 && threadIdx.x >= 32 && threadIdx.x < 32 + (PF > 1 ? 64 : 1)) {
+        // L2 prefetch of the inputs of the tile about one resident wave ahead (warp 1;
+        // thread 0 issues the CLC request): its block scales (one thread, 128-B lines)
+        // and, PF > 1, its codes (64 threads x one 128-B line)
+        const int64_t pt = tile + P.prefetch_ahead;
+        if (pt < P.total_tiles) {
+          int lo = cur, hi = P.count - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (pt < P.t[mid].tile_end) hi = mid; else lo = mid + 1;
+          }
+          const TensorDesc& pd = P.t[lo];
+          const int64_t pe = (pt - (lo == 0 ? 0 : P.t[lo - 1].tile_end)) * TILE;
+          if (threadIdx.x == 32) {
+            const int64_t b0 = pe >> pd.bs_shift;
+            const int64_t nb = (pd.n + (int64_t(1) << pd.bs_shift) - 1) >> pd.bs_shift;
+            const int64_t b1 = min(nb, b0 + ((TILE - 1) >> pd.bs_shift) + 1);
+            const char* a = pd.absmax ? reinterpret_cast<const char*>(pd.absmax + b0)
+                                      : reinterpret_cast<const char*>(pd.qabsmax + b0);
+            const int64_t bytes = (b1 - b0) * (pd.absmax ? 4 : 1);
+            for (int64_t o = 0; o < bytes; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(a + o));
+          } else if (PF > 1) {
+            const int64_t ce = pe + int64_t(threadIdx.x - 32) * 256;   // 128 B of codes = 256 elements
+            if (ce < pd.n) asm volatile("prefetch.global.L2 [%0];" ::"l"(pd.packed + (ce >> 1)));
+          }
+        }
+      }
       const bool full = d.vec_ok && e_tile + TILE <= d.n;
       float* ss = sscale[DB ? (it & 1) : 0];
       // EARLY (small launches, ~one wave of tiles): code loads first -- they do not
@@ -448,6 +477,8 @@ static KernelFn kernel_for(int v) {
     case 12: return dequant_kernel<OUT, 8, 4, false, true, true, true, false, NF4_MAX_BATCH, false, true>;
     case 13: return dequant_kernel<OUT, 8, 2, false, true, true, true>;
     case 14: return dequant_kernel<OUT, 8, 4, false, true, true, true, false, NF4_MAX_BATCH, false, false, 1>;
+    case 15: return dequant_kernel<OUT, 8, 4, false, true, true, true, false, NF4_MAX_BATCH, false, false, 0, 1>;
+    case 16: return dequant_kernel<OUT, 8, 4, false, true, true, true, false, NF4_MAX_BATCH, false, false, 0, 2>;
     default: return dequant_kernel<OUT, 8, 4, false, true, true, true, true>;
   }
 }
@@ -491,7 +522,7 @@ static void launch_small(const BatchParams& P, int out, int grid, cudaStream_t s
   BatchParamsT<MAXB> Q;
   Q.total_tiles = P.total_tiles;
   Q.count = P.count;
-  Q.pad_ = 0;
+  Q.prefetch_ahead = 0;
   for (int i = 0; i < 16; ++i) Q.lut[i] = P.lut[i];
   for (int i = 0; i < P.count; ++i) Q.t[i] = P.t[i];
   // about two resident waves of tiles or fewer: latency-bound, issue code loads first
@@ -583,7 +614,7 @@ static nf4_status launch_batch(const nf4_tensor* ts, int count, int out, const f
   }
   BatchParams P;
   P.count = 0;
-  P.pad_ = 0;
+  P.prefetch_ahead = (v == 15 || v == 16) ? int32_t(occupancy(v, out) * sm_count()) : 0;
   for (int i = 0; i < 16; ++i) P.lut[i] = lut[i];
   int64_t tiles = 0;
   for (int i = 0; i < count; ++i) {

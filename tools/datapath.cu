@@ -110,9 +110,11 @@ __global__ void __launch_bounds__(1024, 1) k_dp(int iters, int nw, unsigned long
       v = v * 1664525u + 1013904223u + w[3];
     } else {   // 5, 6: F1's inner loop
       uint32_t o[16];
+      // 4 distinct code words per iteration (F1: one LDS.128 of codes per 32 weights)
+      const uint32_t cw[4] = {v, v * 3u + 1u, v ^ 0x5A5A5A5Au, (v >> 7) | (v << 25)};
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
-        const uint32_t byte = __byte_perm(v ^ w[q & 3], 0u, 0x4440u + (q & 3));
+        const uint32_t byte = __byte_perm(cw[q >> 2], 0u, 0x4440u + (q & 3));
         uint64_t r, p;
         asm volatile("ld.shared.b64 %0, [%1];" : "=l"(r) : "r"(tab + byte * 128u));
         asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(p) : "l"(r), "l"(aa));
@@ -130,7 +132,7 @@ __global__ void __launch_bounds__(1024, 1) k_dp(int iters, int nw, unsigned long
 #pragma unroll
         for (int q = 0; q < 16; ++q) w[q & 3] ^= o[q];
       }
-      v = v * 1664525u + 1013904223u;
+      v = v * 1664525u + 1013904223u + (MODE == 6 ? w[0] : 0u);
     }
   }
   const unsigned long long t1 = clock64();
