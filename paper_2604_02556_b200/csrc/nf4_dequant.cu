@@ -73,6 +73,8 @@ static const Variant kVariants[] = {
     {"v2u4sxcw", 8, 4, false, true, true, true},     // 14: v2u4sxc with write-back (default-policy) stores
     {"v2u4sxcf", 8, 4, false, true, true, true},     // 15: v2u4sxc + L2 prefetch of the scales one wave ahead
     {"v2u4sxcF", 8, 4, false, true, true, true},     // 16: v2u4sxc + L2 prefetch of scales and codes one wave ahead
+    {"v2u4r2sxc", 8, 8, false, true, true, true},    // 17: 32768-element tiles done as 2 rounds of v2u4sxc's
+                                                     //     loads/stores (per-tile scale decode, barriers, CLC halved)
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 constexpr int kDefaultVariant = 8;   // v2u4sxc: best measured on B200 (profiles/r01_variants.md)
@@ -81,7 +83,7 @@ constexpr int kDefaultVariant = 8;   // v2u4sxc: best measured on B200 (profiles
 #define NF4_QUARTER_TILE_WAVES 4
 #endif
 constexpr int kQuarterTileWaves = NF4_QUARTER_TILE_WAVES;
-constexpr int kMaxTileBlocks = 256;  // TILE / 64 for the 16384-element tiles using sscale
+constexpr int kMaxTileBlocks = 512;  // TILE / 64 for the largest (32768-element) tiles using sscale
 
 struct TensorDesc {
   const uint8_t* packed;
@@ -290,16 +292,17 @@ __device__ __forceinline__ int64_t clc_result(const uint4* result) {
 }
 
 template <int OUT, int VEC, int U, bool PERSIST, bool SSCALE, bool PRMT, bool CLC, bool DB = false,
-          int MAXB = NF4_MAX_BATCH, bool EARLY = false, bool PAIR = false, int STH = 0, int PF = 0>
+          int MAXB = NF4_MAX_BATCH, bool EARLY = false, bool PAIR = false, int STH = 0, int PF = 0, int R = 1>
 __global__ void __launch_bounds__(kThreads) dequant_kernel(const __grid_constant__ BatchParamsT<MAXB> P) {
   constexpr int GROUP = 2 * VEC;                      // elements per thread-group
-  constexpr int64_t TILE = int64_t(kThreads) * GROUP * U;
+  constexpr int64_t SUBTILE = int64_t(kThreads) * GROUP * U;   // one round of loads / stores
+  constexpr int64_t TILE = SUBTILE * R;                        // R rounds share one scale decode
   constexpr int NBUF = DB ? 2 : 1;                    // scale cache / CLC response slots
   static_assert(!SSCALE || TILE / 64 <= kMaxTileBlocks, "tile too large for the scale cache");
   static_assert(!DB || (SSCALE && CLC), "double buffering needs the per-tile barrier of sscale");
   // A1: stage the 16-entry table in shared memory (16 banks, conflict-free).
   __shared__ float lut[16];
-  __shared__ float sscale[NBUF][SSCALE ? kMaxTileBlocks : 1];
+  __shared__ float sscale[NBUF][SSCALE ? int(TILE / 64) : 1];
   __shared__ __align__(16) uint4 clc_res[NBUF];
   __shared__ __align__(8) uint64_t clc_bar[NBUF];
   if (threadIdx.x < 16) lut[threadIdx.x] = P.lut[threadIdx.x];  // kernel-parameter (constant) bank -> smem
@@ -399,7 +402,11 @@ __global__ void __launch_bounds__(kThreads) dequant_kernel(const __grid_constant
         const int64_t b0 = e_tile >> d.bs_shift;
         const int64_t nb = (d.n + (int64_t(1) << d.bs_shift) - 1) >> d.bs_shift;
         const int nblk = int(((TILE - 1) >> d.bs_shift) + 1);
-        if (int(threadIdx.x) < nblk && b0 + threadIdx.x < nb) ss[threadIdx.x] = block_scale(d, b0 + threadIdx.x);
+        if (R == 1) {
+          if (int(threadIdx.x) < nblk && b0 + threadIdx.x < nb) ss[threadIdx.x] = block_scale(d, b0 + threadIdx.x);
+        } else {
+          for (int i = threadIdx.x; i < nblk && b0 + i < nb; i += kThreads) ss[i] = block_scale(d, b0 + i);
+        }
         __syncthreads();
       }
       auto scale_of = [&](int64_t e0) -> float {
@@ -407,28 +414,32 @@ __global__ void __launch_bounds__(kThreads) dequant_kernel(const __grid_constant
       };
 
       if (full) {
-        if (!EARLY) {
+#pragma unroll 1
+        for (int r = 0; r < R; ++r) {
+          const int64_t e_sub = e_tile + r * SUBTILE;
+          if (!EARLY || r > 0) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const int64_t e0 = e_sub + int64_t(u * kThreads + threadIdx.x) * GROUP;
+              q[u] = ld_codes<VEC>(d.packed + (e0 >> 1));
+            }
+          }
+          float a[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) a[u] = scale_of(e_sub + int64_t(u * kThreads + threadIdx.x) * GROUP);
 #pragma unroll
           for (int u = 0; u < U; ++u) {
-            const int64_t e0 = e_tile + int64_t(u * kThreads + threadIdx.x) * GROUP;
-            q[u] = ld_codes<VEC>(d.packed + (e0 >> 1));
+            const int64_t e0 = e_sub + int64_t(u * kThreads + threadIdx.x) * GROUP;
+            uint32_t w[OutWords<OUT, VEC>::value];
+            if constexpr (PAIR)
+              decode_group_pair<OUT, VEC>(ptab_lane, q[u], a[u], w);
+            else
+              decode_group<OUT, VEC, PRMT>(lut, q[u], a[u], w);
+            st_group<OutWords<OUT, VEC>::value, STH>(out_at<OUT>(d.out, e0), w);
           }
         }
-        float a[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) a[u] = scale_of(e_tile + int64_t(u * kThreads + threadIdx.x) * GROUP);
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int64_t e0 = e_tile + int64_t(u * kThreads + threadIdx.x) * GROUP;
-          uint32_t w[OutWords<OUT, VEC>::value];
-          if constexpr (PAIR)
-            decode_group_pair<OUT, VEC>(ptab_lane, q[u], a[u], w);
-          else
-            decode_group<OUT, VEC, PRMT>(lut, q[u], a[u], w);
-          st_group<OutWords<OUT, VEC>::value, STH>(out_at<OUT>(d.out, e0), w);
-        }
       } else {
-        for (int u = 0; u < U; ++u) {
+        for (int u = 0; u < U * R; ++u) {
           const int64_t e0 = e_tile + int64_t(u * kThreads + threadIdx.x) * GROUP;
           if (e0 >= d.n) break;
           const float a = scale_of(e0);  // GROUP | blocksize: one block per group
@@ -479,6 +490,7 @@ static KernelFn kernel_for(int v) {
     case 14: return dequant_kernel<OUT, 8, 4, false, true, true, true, false, NF4_MAX_BATCH, false, false, 1>;
     case 15: return dequant_kernel<OUT, 8, 4, false, true, true, true, false, NF4_MAX_BATCH, false, false, 0, 1>;
     case 16: return dequant_kernel<OUT, 8, 4, false, true, true, true, false, NF4_MAX_BATCH, false, false, 0, 2>;
+    case 17: return dequant_kernel<OUT, 8, 4, false, true, true, true, false, NF4_MAX_BATCH, false, false, 0, 0, 2>;
     default: return dequant_kernel<OUT, 8, 4, false, true, true, true, true>;
   }
 }

@@ -339,6 +339,14 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* m
 #ifndef NF4_GEMM_PAIR_ROW
 #define NF4_GEMM_PAIR_ROW 128
 #endif
+// Register-table lookups (4-warp / BN = 16 producers, byte-pair path): of the 8 code
+// words of a 64-weight chunk, this many are decoded from a per-chunk register table
+// (PRMT byte planes of the 16 pre-scaled 16-bit levels) instead of the shared-memory
+// pair table -- ALU work in place of shared-memory wavefronts, which bind the kernel.
+// 0: off; 1: the last word of the chunk's second half; 2: the last word of each half.
+#ifndef NF4_GEMM_REG_WORDS
+#define NF4_GEMM_REG_WORDS 0
+#endif
 template <int BN> __host__ __device__ constexpr bool pair_for() { return NF4_GEMM_PAIR && BN <= NF4_GEMM_PAIR_MAXBN; }
 template <int BN> __host__ __device__ constexpr int pair_table_bytes() { return pair_for<BN>() ? 256 * NF4_GEMM_PAIR_ROW : 0; }
 
@@ -696,6 +704,8 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
               a = __fadd_rn(__fmul_rn(__ldg(c2 + sc.s[q]), sc.a2[q]), offset);
             }
             const uint64_t aa = f32x2_splat(a);
+            constexpr bool kReg = NF4_GEMM_REG_WORDS > 0 && kProducerWarps == 4 && pair_for<BN>() &&
+                                  NF4_GEMM_ST_SPLIT != 0;
             // 8-warp groups: this thread's half of the chunk; 4-warp groups: both halves
 #pragma unroll
             for (int hh = half; hh < (kProducerWarps == 8 ? half + 1 : 2); ++hh) {
@@ -707,7 +717,36 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
               if constexpr (pair_for<BN>() && NF4_GEMM_ST_SPLIT != 0) {
 #pragma unroll
                 for (int cc = 0; cc < 4; ++cc) {
-                  if (!NF4_EXP(2)) {
+                  const bool reg_word = kReg && cc == 3 && (NF4_GEMM_REG_WORDS >= 2 || hh == 1);
+                  if (!NF4_EXP(2) && reg_word) {
+                    // 8 weights from the register table: 3-bit plane indices (bit 3 cleared), then
+                    // per byte the plane half chosen by bit 3 (selector i + 4 * bit3), then the
+                    // low/high byte planes interleaved into (element 2j | element 2j+1 << 16)
+                    // register table, built here (short live range under the register cap):
+                    // T[v] = RNE16(fl32(lut[v] * a)), the exact words of the pair-table path, as
+                    // byte planes -- tl[k] byte i = low byte of T[4k+i], th[k] the high bytes
+                    uint32_t tl[4], th[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                      const uint32_t t01 = pack2_rn<BF16>(__fmul_rn(p.lut[4 * k], a), __fmul_rn(p.lut[4 * k + 1], a));
+                      const uint32_t t23 =
+                          pack2_rn<BF16>(__fmul_rn(p.lut[4 * k + 2], a), __fmul_rn(p.lut[4 * k + 3], a));
+                      tl[k] = __byte_perm(t01, t23, 0x6420u);
+                      th[k] = __byte_perm(t01, t23, 0x7531u);
+                    }
+                    const uint32_t x = cw[cc];
+                    const uint32_t s7 = x & 0x77777777u;
+#pragma unroll
+                    for (int hw = 0; hw < 2; ++hw) {
+                      const uint32_t sx = hw ? (s7 >> 16) : s7;
+                      const uint32_t tx = ((hw ? (x >> 17) : (x >> 1)) & 0x4444u) | 0x3210u;
+                      const uint32_t lo = __byte_perm(__byte_perm(tl[0], tl[1], sx), __byte_perm(tl[2], tl[3], sx), tx);
+                      const uint32_t hi = __byte_perm(__byte_perm(th[0], th[1], sx), __byte_perm(th[2], th[3], sx), tx);
+                      // lo/hi byte i <-> nibble i of the half-word: (elem 1, elem 0, elem 3, elem 2)
+                      w[4 * cc + 2 * hw] = __byte_perm(lo, hi, 0x4051u);
+                      w[4 * cc + 2 * hw + 1] = __byte_perm(lo, hi, 0x6273u);
+                    }
+                  } else if (!NF4_EXP(2)) {
 #pragma unroll
                     for (int jj = 0; jj < 4; ++jj) {
                       // row of byte jj of the word, this lane's copy
