@@ -76,7 +76,25 @@ namespace gemm {
 #endif
 template <int BN> __host__ __device__ constexpr int wpg_for() { return BN <= NF4_GEMM_W4_MAXBN ? 4 : 8; }
 template <int BN> __host__ __device__ constexpr int groups_for() { return BN <= NF4_GEMM_W4_MAXBN ? NF4_GEMM_W4_GROUPS : NF4_GEMM_GROUPS; }
-template <int BN> __host__ __device__ constexpr int slots_for() { return BN <= NF4_GEMM_W4_MAXBN ? NF4_GEMM_W4_SLOTS : groups_for<BN>(); }
+// 8-warp groups (BN >= 32): NF4_GEMM_WIDE_SLOTS = 1 gives them every A slot TMEM and the code
+// stages allow (min(CST, (512 - accumulators) / (SUB * 32)) >= G) instead of one per group.
+#ifndef NF4_GEMM_WIDE_SLOTS
+#define NF4_GEMM_WIDE_SLOTS 0
+#endif
+template <int BN> constexpr int sub_for();
+template <int BN> constexpr int cst_for();
+template <int BN> constexpr int nacc_for();
+template <int BN> __host__ __device__ constexpr int slots_for() {
+  if constexpr (BN <= NF4_GEMM_W4_MAXBN) {
+    return NF4_GEMM_W4_SLOTS;
+  } else if constexpr (NF4_GEMM_WIDE_SLOTS != 0) {
+    constexpr int tm = (512 - nacc_for<BN>() * (BN < 32 ? 32 : BN)) / (sub_for<BN>() * 32);
+    constexpr int s = tm < cst_for<BN>() ? tm : cst_for<BN>();
+    return s > groups_for<BN>() ? s : groups_for<BN>();
+  } else {
+    return groups_for<BN>();
+  }
+}
 constexpr int kCodeBytes = 32;              // packed bytes per row per k-chunk
 constexpr int kChunk = 64;          // k elements per stage (= one 128 B swizzle row in 16-bit)
 constexpr int kRowBytes = 128;
