@@ -11,6 +11,8 @@
 //   5  F1's inner loop: 16 x (PRMT, LDS.64, FMUL2, cvt.bf16x2) + 2 tcgen05.st.x8
 //   6  mode 5 without the stores (words folded into a sink)
 //   7  tcgen05.st.16x256b.x2 only (2 per iteration = 32 columns... 16 lanes x 256 b x 2)
+//   8  16 SHFL.IDX table lookups (lane i holds level i & 15, source lane = 4-bit code)
+//   9  8 SHFL + 8 LDS.64;  10  16 SHFL + 16 LDS.64 (do shuffles share the LDS data path?)
 // nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o datapath datapath.cu
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -108,6 +110,26 @@ __global__ void __launch_bounds__(1024, 1) k_dp(int iters, int nw, unsigned long
         st_wait();
       }
       v = v * 1664525u + 1013904223u + w[3];
+    } else if (MODE == 8 || MODE == 9 || MODE == 10) {
+      // 8: 16 SHFL.IDX lookups (lane i holds NF4[i & 15]; source lane = a 4-bit code)
+      // 9: 8 LDS.64 + 8 SHFL per iteration; 10: 16 LDS.64 + 16 SHFL
+      const float tabv = 1.0f + 0.01f * float(lane & 15);
+#pragma unroll
+      for (int q = 0; q < (MODE == 10 ? 16 : MODE == 9 ? 8 : 16); ++q) {
+        const uint32_t idx = (v >> (2 * q)) & 15u;
+        const float r = __shfl_sync(0xffffffffu, tabv, int(idx));
+        w[q] ^= __float_as_uint(r);
+      }
+      if (MODE == 9 || MODE == 10) {
+#pragma unroll
+        for (int q = 0; q < (MODE == 10 ? 16 : 8); ++q) {
+          const uint32_t byte = (v >> (2 * q + 1)) & 255u;
+          uint64_t r;
+          asm volatile("ld.shared.b64 %0, [%1];" : "=l"(r) : "r"(tab + byte * 128u));
+          w[16 + q] ^= uint32_t(r) ^ uint32_t(r >> 32);
+        }
+      }
+      v = v * 1664525u + 1013904223u + w[3] + w[17];
     } else {   // 5, 6: F1's inner loop
       uint32_t o[16];
       // 4 distinct code words per iteration (F1: one LDS.128 of codes per 32 weights)
@@ -195,6 +217,10 @@ int main() {
     run<2>("16 LDS.64 + 2 st.x8", sms, nw, 16 * 256, 2048, cyc, sink);
     run<5>("F1 inner loop (lookup+FMUL2+cvt+st)", sms, nw, 16 * 256, 2048, cyc, sink);
     run<6>("F1 inner loop without st", sms, nw, 16 * 256, 0, cyc, sink);
+    // SHFL "bytes": 32 lanes x 4 B per instruction, counted in the LDS column
+    run<8>("16 SHFL.IDX lookups", sms, nw, 16 * 128, 0, cyc, sink);
+    run<9>("8 SHFL + 8 LDS.64", sms, nw, 8 * 128 + 8 * 256, 0, cyc, sink);
+    run<10>("16 SHFL + 16 LDS.64", sms, nw, 16 * 128 + 16 * 256, 0, cyc, sink);
   }
   return 0;
 }
