@@ -1290,7 +1290,13 @@ static bool make_map(CUtensorMap* m, CUtensorMapDataType dt, int elem, const voi
 using namespace nf4;
 using namespace nf4::gemm;
 
+// NF4_GEMM_BN8: token tiles of 8 for M <= 8 (tcgen05.mma kind::f16 with M = 128 takes any N
+// multiple of 8): half the X bytes of a 16-wide tile through TMA and the MMA.
+#ifndef NF4_GEMM_BN8
+#define NF4_GEMM_BN8 0
+#endif
 static int pick_bn(int M) {
+  if (NF4_GEMM_BN8 && M <= 8) return 8;
   if (M <= 16) return 16;
   if (M <= 32) return 32;
   if (M <= 64) return 64;
@@ -1592,6 +1598,9 @@ static nf4_status gemm_run(nf4_dtype x_dtype, int32_t M, int32_t blocksize, cons
   if (!zero_fill()) { cudaGetLastError(); return NF4_ERR_CUDA; }
   cudaError_t e;
   switch (bn) {
+#if NF4_GEMM_BN8
+    case 8: e = bf16 ? launch<8, true>(p, maps, grid, s) : launch<8, false>(p, maps, grid, s); break;
+#endif
     case 16: e = bf16 ? launch<16, true>(p, maps, grid, s) : launch<16, false>(p, maps, grid, s); break;
     case 32: e = bf16 ? launch<32, true>(p, maps, grid, s) : launch<32, false>(p, maps, grid, s); break;
     case 64: e = bf16 ? launch<64, true>(p, maps, grid, s) : launch<64, false>(p, maps, grid, s); break;
