@@ -472,6 +472,8 @@ def measure_dequant(args, cfg, rank, world, device, nf4, torch, steps, full=True
     t_build = time.perf_counter()
     ws, tensors, reps = build_store(args, cfg, rank, world, device)
     torch.cuda.synchronize()
+    # inputs are complete (synchronized) before any timed launch: early input reads are safe
+    nf4.nf4_set_early_input_reads(bool(getattr(args, "early_inputs", False)))
     t_build = time.perf_counter() - t_build
     nt = len(tensors)
     alg_step = alg_bytes_of(tensors, c.blocksize, c.dq)        # one pass over the workload
@@ -562,6 +564,7 @@ def measure_dequant(args, cfg, rank, world, device, nf4, torch, steps, full=True
             launches += step()
         end.record(stream)
     torch.cuda.synchronize()
+    nf4.nf4_set_early_input_reads(False)   # back to the library default for anything after the timing
     if world > 1:
         dist.barrier()
     clocks = sampler.stop() if sampler else None
@@ -804,6 +807,7 @@ def run_ours(args, rank, world, local_rank):
                        "out_dtype": c.out_dtype, "algorithmic_bytes_per_step_per_rank": alg_per_step,
                        "algorithmic_bytes_per_step_total": int(r["tot_bytes"]),
                        "launches_per_step": r["launches_per_step"], "kernel_variant": variant,
+                       "early_input_reads": bool(args.early_inputs),
                        "l2": "inputs+outputs per step >> 126 MB L2 (no flush needed)"
                              if not r["cold"] else f"L2-resident workload: {r['reps']} rotating copies "
                                                    f"(> 4 x L2), the {args.steps} timed steps launched back to back "
@@ -895,6 +899,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--variant", default=None, help="dequant kernel variant (name or index)")
     ap.add_argument("--extra-configs", default="cfg2,cfg1", help="comma list measured after the main config (N=1)")
+    ap.add_argument("--early-inputs", action="store_true",
+                    help="nf4_set_early_input_reads(1): inputs read before the PDL wait (include/nf4.h)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sol", action="store_true")

@@ -203,6 +203,22 @@ const char* nf4_status_string(nf4_status s);
  * the bench's gpu_launches count). */
 int32_t nf4_last_launch_count(void);
 
+/* Early input reads (programmatic dependent launch), process-wide, default 0.
+ * The dequantization kernels are launched so that they may start while the
+ * previous kernel on the stream drains.  0: every global access waits for that
+ * kernel (griddepcontrol.wait first).  1: the INPUTS -- packed codes, absmax or
+ * the double-quant state and tables -- are read before the wait, so their DRAM
+ * round trip overlaps the previous kernel's tail; only the stores to `out` wait
+ * (measured mixed: up to -1.5 us per launch for 2^20-2^21 elements, -4% at
+ * 2^26, but +7-16% at 2^22 / 2^24; profiles/r02_early_inputs.md).  Enable it
+ * only when no kernel that can still be running when the call's kernel starts
+ * writes those inputs: the immediately preceding kernel, and any earlier one
+ * chained to it by programmatic dependent launch (this library's kernels are).
+ * A quantize-then-dequantize sequence on one stream does NOT qualify unless an
+ * event or memcpy boundary separates the two.  Takes effect for later calls;
+ * results are identical either way. */
+void nf4_set_early_input_reads(int32_t enable);
+
 #ifdef __cplusplus
 }
 #endif

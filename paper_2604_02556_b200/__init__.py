@@ -30,6 +30,7 @@ __all__ = [
     "nf4_gemm", "nf4_gemm_default_splits", "nf4_gemm_workspace_bytes", "nf4_dequantize_host_batched",
     "nf4_gemm_grouped", "nf4_gemm_grouped_workspace_bytes",
     "nf4_gemm_multi", "nf4_gemm_multi_workspace_bytes", "nf4_gemm_set_early_weight_reads",
+    "nf4_set_early_input_reads",
 ]
 
 
@@ -396,3 +397,9 @@ def nf4_gemm_multi(problems, *, M: int, blocksize: int = 64, x_dtype="bf16", y_d
 
 def nf4_gemm_set_early_weight_reads(enable: bool) -> None:
     load().nf4_gemm_set_early_weight_reads(1 if enable else 0)
+
+
+def nf4_set_early_input_reads(enable: bool) -> None:
+    """Dequantization kernels read their inputs before waiting for the previous
+    kernel on the stream (contract in include/nf4.h); default off."""
+    load().nf4_set_early_input_reads(1 if enable else 0)

@@ -34,6 +34,7 @@ EXPORTS = [
     "nf4_gemm", "nf4_gemm_default_splits", "nf4_gemm_workspace_bytes", "nf4_dequantize_host_batched",
     "nf4_gemm_grouped", "nf4_gemm_grouped_workspace_bytes",
     "nf4_gemm_multi", "nf4_gemm_multi_workspace_bytes", "nf4_gemm_set_early_weight_reads",
+    "nf4_set_early_input_reads",
 ]
 
 
@@ -107,6 +108,7 @@ def load() -> ctypes.CDLL:
             "nf4_gemm_multi_workspace_bytes": ([i32, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
                                                 i32], i64),
             "nf4_gemm_set_early_weight_reads": ([i32], None),
+            "nf4_set_early_input_reads": ([i32], None),
             "nf4_dequantize_ex": ([P, P, ctypes.POINTER(DQState), i64, i32, P, i32, P, P], st),
             "nf4_dequantize_batched_ex": ([ctypes.POINTER(TensorDesc), i32, P, i32, P], st),
             "nf4_status_string": ([st], ctypes.c_char_p),

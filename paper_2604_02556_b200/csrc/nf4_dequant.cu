@@ -108,6 +108,8 @@ struct BatchParamsT {
   int64_t total_tiles;
   int32_t count;
   int32_t prefetch_ahead; // PF variants: L2-prefetch the inputs of tile + prefetch_ahead (0: off)
+  int32_t early_inputs;   // 1: read codes and scales before griddepcontrol.wait (nf4_set_early_input_reads)
+  int32_t pad2_;
   float lut[16];          // the 16-entry codebook (NF4 unless nf4_dequantize_ex supplies one)
   TensorDesc t[MAXB];
 };
@@ -326,7 +328,12 @@ __global__ void __launch_bounds__(kThreads) dequant_kernel(const __grid_constant
   // shared memory, so it may overlap the previous kernel's tail; inputs and the
   // output buffer are touched only after the previous grid has completed.
   if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // early_inputs: the inputs (codes, scales, tables) are read before the previous
+  // kernel on the stream has completed -- its DRAM round trip overlaps that kernel's
+  // tail -- and only the stores wait (griddepcontrol.wait before every tile's first
+  // store; a no-op once satisfied).  The caller guarantees the previous kernel does not
+  // write this launch's inputs (include/nf4.h).
+  if (!P.early_inputs) asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
 
   int cur = 0;
@@ -427,6 +434,7 @@ __global__ void __launch_bounds__(kThreads) dequant_kernel(const __grid_constant
           float a[U];
 #pragma unroll
           for (int u = 0; u < U; ++u) a[u] = scale_of(e_sub + int64_t(u * kThreads + threadIdx.x) * GROUP);
+          if (P.early_inputs) asm volatile("griddepcontrol.wait;" ::: "memory");   // out may be in use
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const int64_t e0 = e_sub + int64_t(u * kThreads + threadIdx.x) * GROUP;
@@ -439,6 +447,7 @@ __global__ void __launch_bounds__(kThreads) dequant_kernel(const __grid_constant
           }
         }
       } else {
+        if (P.early_inputs) asm volatile("griddepcontrol.wait;" ::: "memory");
         for (int u = 0; u < U * R; ++u) {
           const int64_t e0 = e_tile + int64_t(u * kThreads + threadIdx.x) * GROUP;
           if (e0 >= d.n) break;
@@ -496,6 +505,7 @@ static KernelFn kernel_for(int v) {
 }
 
 static std::atomic<int> g_variant{-1};
+static std::atomic<int32_t> g_early_inputs{0};
 
 static int current_variant() {
   int v = g_variant.load(std::memory_order_relaxed);
@@ -535,6 +545,8 @@ static void launch_small(const BatchParams& P, int out, int grid, cudaStream_t s
   Q.total_tiles = P.total_tiles;
   Q.count = P.count;
   Q.prefetch_ahead = 0;
+  Q.early_inputs = P.early_inputs;
+  Q.pad2_ = 0;
   for (int i = 0; i < 16; ++i) Q.lut[i] = P.lut[i];
   for (int i = 0; i < P.count; ++i) Q.t[i] = P.t[i];
   // about two resident waves of tiles or fewer: latency-bound, issue code loads first
@@ -627,6 +639,8 @@ static nf4_status launch_batch(const nf4_tensor* ts, int count, int out, const f
   BatchParams P;
   P.count = 0;
   P.prefetch_ahead = (v == 15 || v == 16) ? int32_t(occupancy(v, out) * sm_count()) : 0;
+  P.early_inputs = g_early_inputs.load(std::memory_order_relaxed);
+  P.pad2_ = 0;
   for (int i = 0; i < 16; ++i) P.lut[i] = lut[i];
   int64_t tiles = 0;
   for (int i = 0; i < count; ++i) {
@@ -780,3 +794,6 @@ extern "C" int32_t nf4_set_kernel_variant(int32_t v) {
   return v;
 }
 extern "C" int32_t nf4_get_kernel_variant(void) { return current_variant(); }
+extern "C" void nf4_set_early_input_reads(int32_t enable) {
+  g_early_inputs.store(enable ? 1 : 0, std::memory_order_relaxed);
+}

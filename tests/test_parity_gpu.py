@@ -576,3 +576,47 @@ def test_quarter_tile_launches(nf4, orc):
     torch.cuda.synchronize()
     for d, ref in zip(descs, refs):
         assert np.array_equal(host16(d.out), ref)
+
+
+@pytest.mark.parametrize("dq", [False, True])
+def test_early_input_reads_bit_exact(nf4, orc, dq):
+    """nf4_set_early_input_reads(1): inputs read before griddepcontrol.wait, stores
+    after it.  A chain of PDL launches where each launch's OUTPUT buffer is still
+    being written/read by the previous launches (out buffers reused round-robin, a
+    zero-fill kernel between) must give the oracle's bytes: the early reads touch
+    only inputs, never `out`.  Default sizes, quarter tiles and the element path."""
+    import torch
+    cases = [(5 * TILE + 77, 64), (3000, 128), (40 * TILE, 64), (2 * TILE, 4096)]
+    data = []
+    for i, (n, bs) in enumerate(cases):
+        packed, kw = _inputs(n, bs, dq, 700 + i)
+        data.append((n, bs, packed, kw, _oracle(orc, packed, kw, n, bs, "f16")))
+    nf4.nf4_set_early_input_reads(True)
+    try:
+        s = torch.cuda.Stream()
+        outs = [torch.empty(max(n for n, *_ in data), dtype=torch.float16, device="cuda") for _ in range(2)]
+        dev_in = []
+        for n, bs, packed, kw, _ in data:
+            dev_in.append((dev(packed), {k: (dev(v) if isinstance(v, np.ndarray) else v) for k, v in kw.items()}))
+        torch.cuda.synchronize()
+        results = []
+        with torch.cuda.stream(s):
+            for rep in range(3):
+                for i, (n, bs, packed, kw, ref) in enumerate(data):
+                    out = outs[(rep * len(data) + i) % 2]
+                    out.fill_(0.0)                       # a kernel writing `out` right before the launch
+                    pk, k2 = dev_in[i]
+                    if dq:
+                        d = nf4.DQ(k2["qabsmax"], k2["code2"], k2["absmax2"], k2["offset"])
+                        nf4.nf4_dequantize(pk, None, d, n=n, blocksize=bs, out_dtype="f16", out=out[:n], stream=s)
+                    else:
+                        nf4.nf4_dequantize(pk, k2["absmax"], None, n=n, blocksize=bs, out_dtype="f16", out=out[:n],
+                                           stream=s)
+                    got = torch.empty(n, dtype=torch.int16, device="cuda")
+                    got.copy_(out[:n].view(torch.int16))
+                    results.append((rep, i, got, ref))
+        s.synchronize()
+        for rep, i, got, ref in results:
+            assert np.array_equal(got.cpu().numpy().view(np.uint16), ref), (rep, i)
+    finally:
+        nf4.nf4_set_early_input_reads(False)

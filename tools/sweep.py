@@ -36,9 +36,13 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--method", default="graph", choices=["graph", "events"])
     ap.add_argument("--launches", type=int, default=64, help="graph method: launches per replay")
+    ap.add_argument("--early-inputs", action="store_true", help="nf4_set_early_input_reads(1)")
+    ap.add_argument("--bs", default="64,128,256,4096")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     nf4.load()
+    if args.early_inputs:
+        nf4.nf4_set_early_input_reads(True)
     # L2 flush by READING 512 MB (a write-based flush leaves 256 MB of dirty lines whose
     # lazy write-back would then be charged to the timed launch)
     flush = torch.ones(512 << 20, dtype=torch.uint8, device="cuda")
@@ -52,7 +56,7 @@ def main():
     rows = []
     print("| bs | dtype | n | cold/hot | us | GB/s | % of measured copy | Gelem/s |")
     print("|---|---|---|---|---|---|---|---|")
-    for bs in (64, 128, 256, 4096):
+    for bs in (int(b) for b in args.bs.split(",")):
         nb = nmax // bs
         if args.dq:
             q = torch.empty(nb, dtype=torch.uint8, device="cuda")
