@@ -29,8 +29,12 @@ def main():
     code2 = syn.dynamic_map_code2()
     variants = nf4.nf4_kernel_variants()
     only_default = os.environ.get("NF4_SANITIZE_DEFAULT_ONLY") == "1"
-    for v in ([nf4.nf4_get_kernel_variant()] if only_default else range(len(variants))):
+    default_v = nf4.nf4_get_kernel_variant()
+    passes = [(v, False) for v in ([default_v] if only_default else range(len(variants)))] + [(default_v, True)]
+    for v, early in passes:     # the last pass: early input reads (nf4_set_early_input_reads)
         nf4.nf4_set_kernel_variant(v)
+        torch.cuda.synchronize()
+        nf4.nf4_set_early_input_reads(early)
         for n in (1, 31, 16384 + 77, 3 * 16384):
             for dq in (False, True):
                 nb = -(-n // 64)
@@ -46,6 +50,8 @@ def main():
                 torch.cuda.synchronize()
                 ref = oracle.dequantize(packed, n, 64, oracle.OUT_BF16, **kw)
                 bad += int(not np.array_equal(out.view(torch.int16).cpu().numpy().view(np.uint16), ref))
+    nf4.nf4_set_early_input_reads(False)
+    nf4.nf4_set_kernel_variant(default_v)
     # unaligned output
     n = 5000
     packed = syn.hash_packed(3, 0, n // 2)
