@@ -377,6 +377,31 @@ def measure_sol(nf4, torch, in_bytes=2 << 30, reps=10):
     return round(5 * in_bytes / (ms * 1e-3) / 1e9, 1)
 
 
+def pcie_link_rates(torch, nbytes=1 << 30):
+    """Plain pinned-host <-> HBM copy rates (torch copy_, CUDA events, best of 3) --
+    the ceiling of the e2e path, whose outputs must cross this link."""
+    try:
+        h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+        d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        s = torch.cuda.current_stream()
+        res = {}
+        for name, fn in (("d2h_gbs", lambda: h.copy_(d, non_blocking=True)),
+                         ("h2d_gbs", lambda: d.copy_(h, non_blocking=True))):
+            best = 1e30
+            for _ in range(3):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(s)
+                fn()
+                b.record(s)
+                b.synchronize()
+                best = min(best, a.elapsed_time(b))
+            res[name] = round(nbytes / (best * 1e-3) / 1e9, 2)
+        del h, d
+        return res
+    except Exception as e:   # pinned allocation refused: report nothing rather than fail the bench
+        return {"error": str(e)[:120]}
+
+
 def run_e2e(nf4, torch, ws, args, max_host_bytes, device=None, world=1):
     """Same metric through nf4_dequantize_host_batched: pinned host inputs -> HBM
     -> kernel -> pinned host outputs, copies inside the timed region."""
@@ -435,7 +460,13 @@ def run_e2e(nf4, torch, ws, args, max_host_bytes, device=None, world=1):
     dt_ms, alg_all, elems_all = reduce_over_ranks(dt * 1e3, float(alg), float(sum(it[3] for it in items)),
                                                   device if device is not None else "cpu", world)
     dt = dt_ms * 1e-3
+    link = pcie_link_rates(torch)
+    if link and "d2h_gbs" in link:
+        # the outputs (2 B per element, ~80% of the step's bytes) cross PCIe device->host
+        link["e2e_d2h_gbs"] = round(d2h / (dt_ms * 1e-3) / 1e9, 2)
+        link["e2e_d2h_frac_of_link"] = round(link["e2e_d2h_gbs"] / link["d2h_gbs"], 3)
     return {"value": round(alg_all / dt / 1e9, 2), "unit": UNIT, "h2d_bytes_per_step": int(h2d) * world,
+            "pcie": link,
             "d2h_bytes_per_step": int(d2h) * world, "ms_per_step": round(dt * 1e3, 2),
             "gelem_per_s": round(elems_all / dt / 1e9, 3),
             "sample": f"first {len(chosen)} of {len(ws.entries)} tensors per rank "
