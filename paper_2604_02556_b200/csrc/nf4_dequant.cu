@@ -54,6 +54,7 @@ struct Variant {
   const char* name;
   int vec, unroll;
   bool persist, sscale, prmt, clc;
+  int threads = kThreads;   // CTA size
 };
 static const Variant kVariants[] = {
     {"v2u4", 8, 4, false, false, false, false},      // 0
@@ -75,6 +76,9 @@ static const Variant kVariants[] = {
     {"v2u4sxcF", 8, 4, false, true, true, true},     // 16: v2u4sxc + L2 prefetch of scales and codes one wave ahead
     {"v2u4r2sxc", 8, 8, false, true, true, true},    // 17: 32768-element tiles done as 2 rounds of v2u4sxc's
                                                      //     loads/stores (per-tile scale decode, barriers, CLC halved)
+    {"v2u4sxcp512", 8, 4, false, true, true, true, 512},  // 18: the byte-pair table (v2u4sxcp) in 512-thread CTAs:
+                                                          //     4 x 32 KB tables per SM, full occupancy
+    {"v2u4sxc512", 8, 4, false, true, true, true, 512},   // 19: the default kernel in 512-thread CTAs
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 constexpr int kDefaultVariant = 8;   // v2u4sxc: best measured on B200 (profiles/r01_variants.md)
@@ -294,10 +298,11 @@ __device__ __forceinline__ int64_t clc_result(const uint4* result) {
 }
 
 template <int OUT, int VEC, int U, bool PERSIST, bool SSCALE, bool PRMT, bool CLC, bool DB = false,
-          int MAXB = NF4_MAX_BATCH, bool EARLY = false, bool PAIR = false, int STH = 0, int PF = 0, int R = 1>
-__global__ void __launch_bounds__(kThreads) dequant_kernel(const __grid_constant__ BatchParamsT<MAXB> P) {
+          int MAXB = NF4_MAX_BATCH, bool EARLY = false, bool PAIR = false, int STH = 0, int PF = 0, int R = 1,
+          int NT = kThreads>
+__global__ void __launch_bounds__(NT) dequant_kernel(const __grid_constant__ BatchParamsT<MAXB> P) {
   constexpr int GROUP = 2 * VEC;                      // elements per thread-group
-  constexpr int64_t SUBTILE = int64_t(kThreads) * GROUP * U;   // one round of loads / stores
+  constexpr int64_t SUBTILE = int64_t(NT) * GROUP * U;   // one round of loads / stores
   constexpr int64_t TILE = SUBTILE * R;                        // R rounds share one scale decode
   constexpr int NBUF = DB ? 2 : 1;                    // scale cache / CLC response slots
   static_assert(!SSCALE || TILE / 64 <= kMaxTileBlocks, "tile too large for the scale cache");
@@ -310,7 +315,7 @@ __global__ void __launch_bounds__(kThreads) dequant_kernel(const __grid_constant
   if (threadIdx.x < 16) lut[threadIdx.x] = P.lut[threadIdx.x];  // kernel-parameter (constant) bank -> smem
   extern __shared__ __align__(128) uint8_t ptab[];                // PAIR: kPairBytes of dynamic smem
   if constexpr (PAIR) {
-    for (int i = threadIdx.x; i < 256 * (kPairRow / 16); i += kThreads) {
+    for (int i = threadIdx.x; i < 256 * (kPairRow / 16); i += NT) {
       const int b = i / (kPairRow / 16);
       const float h = P.lut[b >> 4], l = P.lut[b & 15];
       *reinterpret_cast<float4*>(ptab + 16 * i) = make_float4(h, l, h, l);
@@ -397,7 +402,7 @@ __global__ void __launch_bounds__(kThreads) dequant_kernel(const __grid_constant
       if (EARLY && full) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const int64_t e0 = e_tile + int64_t(u * kThreads + threadIdx.x) * GROUP;
+          const int64_t e0 = e_tile + int64_t(u * NT + threadIdx.x) * GROUP;
           q[u] = ld_codes<VEC>(d.packed + (e0 >> 1));
         }
       }
@@ -412,7 +417,7 @@ __global__ void __launch_bounds__(kThreads) dequant_kernel(const __grid_constant
         if (R == 1) {
           if (int(threadIdx.x) < nblk && b0 + threadIdx.x < nb) ss[threadIdx.x] = block_scale(d, b0 + threadIdx.x);
         } else {
-          for (int i = threadIdx.x; i < nblk && b0 + i < nb; i += kThreads) ss[i] = block_scale(d, b0 + i);
+          for (int i = threadIdx.x; i < nblk && b0 + i < nb; i += NT) ss[i] = block_scale(d, b0 + i);
         }
         __syncthreads();
       }
@@ -427,17 +432,17 @@ __global__ void __launch_bounds__(kThreads) dequant_kernel(const __grid_constant
           if (!EARLY || r > 0) {
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-              const int64_t e0 = e_sub + int64_t(u * kThreads + threadIdx.x) * GROUP;
+              const int64_t e0 = e_sub + int64_t(u * NT + threadIdx.x) * GROUP;
               q[u] = ld_codes<VEC>(d.packed + (e0 >> 1));
             }
           }
           float a[U];
 #pragma unroll
-          for (int u = 0; u < U; ++u) a[u] = scale_of(e_sub + int64_t(u * kThreads + threadIdx.x) * GROUP);
+          for (int u = 0; u < U; ++u) a[u] = scale_of(e_sub + int64_t(u * NT + threadIdx.x) * GROUP);
           if (P.early_inputs) asm volatile("griddepcontrol.wait;" ::: "memory");   // out may be in use
 #pragma unroll
           for (int u = 0; u < U; ++u) {
-            const int64_t e0 = e_sub + int64_t(u * kThreads + threadIdx.x) * GROUP;
+            const int64_t e0 = e_sub + int64_t(u * NT + threadIdx.x) * GROUP;
             uint32_t w[OutWords<OUT, VEC>::value];
             if constexpr (PAIR)
               decode_group_pair<OUT, VEC>(ptab_lane, q[u], a[u], w);
@@ -449,7 +454,7 @@ __global__ void __launch_bounds__(kThreads) dequant_kernel(const __grid_constant
       } else {
         if (P.early_inputs) asm volatile("griddepcontrol.wait;" ::: "memory");
         for (int u = 0; u < U * R; ++u) {
-          const int64_t e0 = e_tile + int64_t(u * kThreads + threadIdx.x) * GROUP;
+          const int64_t e0 = e_tile + int64_t(u * NT + threadIdx.x) * GROUP;
           if (e0 >= d.n) break;
           const float a = scale_of(e0);  // GROUP | blocksize: one block per group
           if (d.vec_ok && e0 + GROUP <= d.n) {
@@ -500,6 +505,8 @@ static KernelFn kernel_for(int v) {
     case 15: return dequant_kernel<OUT, 8, 4, false, true, true, true, false, NF4_MAX_BATCH, false, false, 0, 1>;
     case 16: return dequant_kernel<OUT, 8, 4, false, true, true, true, false, NF4_MAX_BATCH, false, false, 0, 2>;
     case 17: return dequant_kernel<OUT, 8, 4, false, true, true, true, false, NF4_MAX_BATCH, false, false, 0, 0, 2>;
+    case 18: return dequant_kernel<OUT, 8, 4, false, true, true, true, false, NF4_MAX_BATCH, false, true, 0, 0, 1, 512>;
+    case 19: return dequant_kernel<OUT, 8, 4, false, true, true, true, false, NF4_MAX_BATCH, false, false, 0, 0, 1, 512>;
     default: return dequant_kernel<OUT, 8, 4, false, true, true, true, true>;
   }
 }
@@ -520,15 +527,17 @@ static int current_variant() {
   return v;
 }
 
-static int64_t tile_elems(int v) { return int64_t(kThreads) * 2 * kVariants[v].vec * kVariants[v].unroll; }
+static int64_t tile_elems(int v) { return int64_t(kVariants[v].threads) * 2 * kVariants[v].vec * kVariants[v].unroll; }
+static bool pair_variant(int v) { return v == 12 || v == 18; }
 
 // Launch with programmatic stream serialization (PDL): the kernel executes
 // griddepcontrol.wait before its first global access.
 template <typename Kernel, typename Params>
-static void launch_pdl(Kernel k, int grid, cudaStream_t stream, const Params& P, size_t smem = 0) {
+static void launch_pdl(Kernel k, int grid, cudaStream_t stream, const Params& P, size_t smem = 0,
+                       int threads = kThreads) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(grid));
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(unsigned(threads));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute at[1];
@@ -589,7 +598,8 @@ static int occupancy(int v, int out) {
   if (c == 0) {
     int occ = 0;
     const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &occ, reinterpret_cast<const void*>(kernel_of(out, v)), kThreads, v == 12 ? size_t(kPairBytes) : 0);
+        &occ, reinterpret_cast<const void*>(kernel_of(out, v)), kVariants[v].threads,
+        pair_variant(v) ? size_t(kPairBytes) : 0);
     c = (e == cudaSuccess && occ > 0) ? occ : 4;
   }
   return c;
@@ -670,7 +680,7 @@ static nf4_status launch_batch(const nf4_tensor* ts, int count, int out, const f
     else launch_small<16>(P, out, grid, stream, quarter);
   } else {
     KernelFn fn = kernel_of(out, v);
-    launch_pdl(fn, grid, stream, P, v == 12 ? size_t(kPairBytes) : 0);
+    launch_pdl(fn, grid, stream, P, pair_variant(v) ? size_t(kPairBytes) : 0, kVariants[v].threads);
   }
   const cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) {
