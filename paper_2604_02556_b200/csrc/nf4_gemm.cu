@@ -265,7 +265,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #ifndef NF4_GEMM_EXP_CONST
 #define NF4_GEMM_EXP_CONST 0
 #endif
-#define NF4_EXP(bit) ((NF4_GEMM_EXP_CONST & (bit)) || (NF4_GEMM_DIAG && (p.experiment & (bit))))
+// (the run-time experiment mask only in NF4_GEMM_DIAG >= 2 builds: DIAG = 1 traces at production speed)
+#define NF4_EXP(bit) ((NF4_GEMM_EXP_CONST & (bit)) || (NF4_GEMM_DIAG >= 2 && (p.experiment & (bit))))
 #define NF4_TRACING (NF4_GEMM_DIAG && p.trace != nullptr)
 // per-super-stage event times of CTA 0, slot base + J (J < 80)
 #define NF4_TRACE_J(base, Jv)                                                                       \
@@ -530,16 +531,26 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
     p.trace[1024 + 4 * cta_lin] = gtimer();
     p.trace[1024 + 4 * cta_lin + 2] = smid;
   }
+  if (warp == kTmaWarp && lane == 0) {   // descriptor fetch overlaps the whole prologue
+    for (int i = 0; i < NM && i < p.nmem && i < 8; ++i) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.c[i])) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.x[i])) : "memory");
+    }
+  }
   if (threadIdx.x < 16) lut[threadIdx.x] = p.lut[threadIdx.x];
   if constexpr (pair_for<BN>()) {
     // row b: ROW/8 copies of (NF4[b >> 4], NF4[b & 15]); 16-B stores of two copies
+    // (levels from a register per lane + shuffles, not per-thread indexing of the parameter bank)
     constexpr int kStoresPerRow = NF4_GEMM_PAIR_ROW / 16;
-    for (int i = threadIdx.x; i < 256 * kStoresPerRow; i += blockDim.x) {
-      const int b = i / kStoresPerRow;
-      const float h = p.lut[b >> 4], l = p.lut[b & 15];
-      *reinterpret_cast<float4*>(ptab + 16 * i) = make_float4(h, l, h, l);
+    const float lv = p.lut[lane & 15];
+    for (int i0 = int(threadIdx.x) & ~31; i0 < 256 * kStoresPerRow; i0 += blockDim.x) {   // warp-uniform trip count
+      const int i = i0 + lane;
+      const int b = (i / kStoresPerRow) & 255;
+      const float h = __shfl_sync(0xffffffffu, lv, b >> 4), l = __shfl_sync(0xffffffffu, lv, b & 15);
+      if (i < 256 * kStoresPerRow) *reinterpret_cast<float4*>(ptab + 16 * i) = make_float4(h, l, h, l);
     }
   }
+  if (NF4_TRACING && cta_lin == 0 && threadIdx.x == 0) p.trace[600] = gtimer();   // prologue: table built
 #if NF4_GEMM_HANG_DIAG
   if (threadIdx.x == 0 && blockIdx.x == 0)
     printf("BARS c_full 0x%x x_full 0x%x c_free 0x%x w_full 0x%x a_free 0x%x acc_full 0x%x acc_empty 0x%x CST %d S %d G %d\n",
@@ -561,7 +572,9 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
       mbar_init(&acc_empty[s], kProducerWarps);
       epi_done[s] = 0;
     }
+    if (NF4_TRACING && cta_lin == 0) p.trace[603] = gtimer();   // barriers initialised
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (NF4_TRACING && cta_lin == 0) p.trace[604] = gtimer();   // init fence
     if (p.streamk) {
       const int64_t W = p.total_chunks, NG = gridDim.x;
       const int64_t x0 = sk_bound(blockIdx.x, W, NG, p.align4);
@@ -571,17 +584,13 @@ __global__ void __launch_bounds__(32 * (wpg_for<BN>() * G + 2), 1)
     } else {
       sk_range[0] = sk_range[1] = sk_range[2] = 0;
     }
+    if (NF4_TRACING && cta_lin == 0) p.trace[601] = gtimer();   // stream-K range
   }
   if (warp == kMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_holder))
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  if (warp == kTmaWarp && lane == 0) {
-    for (int i = 0; i < NM && i < p.nmem && i < 8; ++i) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.c[i])) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.x[i])) : "memory");
-    }
+    if (NF4_TRACING && cta_lin == 0 && lane == 0) p.trace[602] = gtimer();   // TMEM allocated
   }
   // Programmatic dependent launch: the next kernel in the stream may start its own
   // prologue as soon as our CTAs leave their SMs.  Only X, y and the workspace
